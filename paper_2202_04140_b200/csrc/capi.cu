@@ -1,0 +1,691 @@
+// C ABI of the B200 evaluator (include/acedag_b200.h): plan ownership,
+// argument validation, kernel dispatch.  No host synchronisation on the hot
+// calls (acedag_eval, acedag_eval_from_positions, acedag_pool*).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/acedag_b200.h"
+#include "graph.h"
+#include "kernels.cuh"
+#include "plan.h"
+#include "pool.cuh"
+
+using namespace acedag;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(ACEDAG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t upload(const std::vector<T>& v) {
+    if (p) { cudaFree(p); p = nullptr; }
+    n = v.size();
+    if (!n) return cudaSuccess;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice);
+  }
+  cudaError_t alloc(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) { cudaFree(p); p = nullptr; }
+    n = count;
+    return cudaMalloc(&p, n * sizeof(T));
+  }
+};
+
+std::vector<int4> label_table(int group, int cap) {
+  std::vector<Label> labs = one_particle_indices(group, cap);
+  std::vector<int4> t(labs.size());
+  for (size_t i = 0; i < labs.size(); ++i) {
+    const Label& L = labs[i];
+    if (group == kT) t[i] = make_int4(L.comp[0], 0, 0, 0);
+    else if (group == kSO2) t[i] = make_int4(L.comp[0], L.comp[1], 0, 0);
+    else t[i] = make_int4(L.comp[0], L.comp[1], L.comp[2], L.ncomp == 4 ? L.comp[3] : 0);
+  }
+  return t;
+}
+
+// per-device constant setup + label tables, created once
+std::mutex g_mu;
+std::map<int, bool> g_norms_ready;
+std::map<std::tuple<int, int, int>, int4*> g_label_cache;
+
+int ensure_norms(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_norms_ready[dev]) return 0;
+  CK(cudaMemcpyToSymbol(dev::c_ylm_norm, kYlmNorm, sizeof(kYlmNorm)));
+  g_norms_ready[dev] = true;
+  return 0;
+}
+
+int device_labels(int dev, int group, int cap, const int4** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(dev, group, cap);
+  auto it = g_label_cache.find(key);
+  if (it != g_label_cache.end()) { *out = it->second; return 0; }
+  std::vector<int4> t = label_table(group, cap);
+  int4* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(1, t.size()) * sizeof(int4)));
+  if (!t.empty()) CK(cudaMemcpy(p, t.data(), t.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  g_label_cache[key] = p;
+  *out = p;
+  return 0;
+}
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+}  // namespace
+
+struct acedag_graph {
+  Graph g;
+};
+
+struct acedag_plan {
+  std::shared_ptr<const Graph> g;
+  int device = 0;
+  int sms = 148;
+  size_t smem_optin = 232448;
+  DevBuf<int32_t> pa, pb;
+  bool has_coef = false;
+  PlanHost host;
+  int U = 0;
+  DevBuf<uint16_t> slot_label, slot_identity;
+  DevBuf<int32_t> used_labels;
+  DevBuf<Op> ops;
+  DevBuf<int32_t> chunk;
+  DevBuf<double> cre, cim;
+  DevBuf<int32_t> nseg;
+  DevBuf<uint16_t> nslots;
+  DevBuf<double> ncre, ncim;
+  DevBuf<double2> gcache;
+  DevBuf<double2> ws_A;
+};
+
+// ====================================================================== API
+extern "C" {
+
+int acedag_abi_version(void) { return ACEDAG_ABI_VERSION; }
+const char* acedag_last_error(void) { return g_err.c_str(); }
+
+int acedag_graph_build(int group, int p, double max_degree, int nu_max, int alg, int n,
+                       acedag_graph** out) {
+  if (!out) return fail(ACEDAG_EINVAL, "out is NULL");
+  try {
+    std::unique_ptr<acedag_graph> h(new acedag_graph);
+    build_graph(h->g, group, p, max_degree, nu_max, alg, n);
+    *out = h.release();
+    return ACEDAG_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(ACEDAG_ENOMEM, "out of host memory building the graph");
+  } catch (const std::exception& e) {
+    return fail(ACEDAG_EINVAL, e.what());
+  }
+}
+
+int acedag_graph_from_parents(int group, int p, double max_degree, int nu_max, int alg, int n,
+                              int64_t n_nodes, int64_t n_seeds, const int32_t* parents,
+                              const uint8_t* aux, acedag_graph** out) {
+  if (!out || !parents) return fail(ACEDAG_EINVAL, "NULL argument");
+  try {
+    std::unique_ptr<acedag_graph> h(new acedag_graph);
+    graph_from_parents(h->g, group, p, max_degree, nu_max, alg, n, n_nodes, n_seeds, parents, aux);
+    *out = h.release();
+    return ACEDAG_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(ACEDAG_ENOMEM, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(ACEDAG_EINVAL, e.what());
+  }
+}
+
+void acedag_graph_destroy(acedag_graph* g) { delete g; }
+
+int acedag_graph_info(const acedag_graph* h, int64_t* n_nodes, int64_t* n_seeds, int64_t* n_targets,
+                      int64_t* n_aux, int32_t* max_order) {
+  if (!h) return fail(ACEDAG_EINVAL, "graph is NULL");
+  const Graph& g = h->g;
+  int64_t aux = 0;
+  int mo = 1;
+  for (size_t i = 0; i < g.tuples.size(); ++i) {
+    aux += g.aux[i];
+    mo = std::max<int>(mo, g.tuples[i].len);
+  }
+  if (n_nodes) *n_nodes = (int64_t)g.tuples.size();
+  if (n_seeds) *n_seeds = g.n_seeds();
+  if (n_targets) *n_targets = (int64_t)g.target_ids().size();
+  if (n_aux) *n_aux = aux;
+  if (max_order) *max_order = mo;
+  return ACEDAG_OK;
+}
+
+int acedag_graph_arrays(const acedag_graph* h, int32_t* parents, uint8_t* aux, int32_t* order,
+                        int32_t* target_ids) {
+  if (!h) return fail(ACEDAG_EINVAL, "graph is NULL");
+  const Graph& g = h->g;
+  for (size_t i = 0; i < g.tuples.size(); ++i) {
+    if (parents) { parents[2 * i] = g.pa[i]; parents[2 * i + 1] = g.pb[i]; }
+    if (aux) aux[i] = g.aux[i];
+    if (order) order[i] = g.tuples[i].len;
+  }
+  if (target_ids) {
+    std::vector<int32_t> t = g.target_ids();
+    std::memcpy(target_ids, t.data(), t.size() * sizeof(int32_t));
+  }
+  return ACEDAG_OK;
+}
+
+int acedag_graph_node_seeds(const acedag_graph* h, int64_t node, int32_t* seeds_out, int32_t capacity) {
+  if (!h || !seeds_out) return fail(ACEDAG_EINVAL, "NULL argument");
+  const Graph& g = h->g;
+  if (node < 0 || node >= (int64_t)g.tuples.size()) return fail(ACEDAG_EINVAL, "node id out of range");
+  const Tuple& t = g.tuples[node];
+  if (capacity < t.len) return fail(ACEDAG_EINVAL, "capacity below the node order");
+  for (int i = 0; i < t.len; ++i) seeds_out[i] = t.id[i];
+  return t.len;
+}
+
+int64_t acedag_graph_find(const acedag_graph* h, const int32_t* seeds, int32_t len) {
+  if (!h || !seeds || len < 1 || len > kMaxOrder) return -1;
+  Tuple t;
+  for (int i = 0; i < len; ++i) {
+    if (seeds[i] < 0 || seeds[i] >= h->g.n_seeds()) return -1;
+    if (i && seeds[i] < seeds[i - 1]) return -1;
+    t.id[t.len++] = (uint16_t)seeds[i];
+  }
+  return h->g.ids.get(t);
+}
+
+int acedag_graph_serialize(const acedag_graph* h, char* buf, int64_t* len) {
+  if (!h || !len) return fail(ACEDAG_EINVAL, "NULL argument");
+  try {
+    std::string s = h->g.serialize();
+    if (buf) {
+      if (*len < (int64_t)s.size()) return fail(ACEDAG_EINVAL, "buffer too small");
+      std::memcpy(buf, s.data(), s.size());
+    }
+    *len = (int64_t)s.size();
+    return ACEDAG_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(ACEDAG_ENOMEM, "out of host memory serializing");
+  }
+}
+
+// ------------------------------------------------------------------ plans
+int acedag_plan_create(const acedag_graph* h, int device, acedag_plan** out) {
+  if (!h || !out) return fail(ACEDAG_EINVAL, "NULL argument");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(ACEDAG_EINVAL, "device ordinal out of range");
+  DevGuard dg(device);
+  std::unique_ptr<acedag_plan> P(new (std::nothrow) acedag_plan);
+  if (!P) return fail(ACEDAG_ENOMEM, "out of host memory");
+  P->g = std::make_shared<const Graph>(h->g);
+  P->device = device;
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  P->smem_optin = (size_t)optin;
+  CK(P->pa.upload(P->g->pa));
+  CK(P->pb.upload(P->g->pb));
+  int rc = ensure_norms(device);
+  if (rc) return rc;
+  *out = P.release();
+  return ACEDAG_OK;
+}
+
+void acedag_plan_destroy(acedag_plan* plan) {
+  if (!plan) return;
+  DevGuard dg(plan->device);
+  delete plan;
+}
+
+int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const double* c_re,
+                                 const double* c_im, int64_t n_coef, int32_t n_out) {
+  if (!P) return fail(ACEDAG_EINVAL, "plan is NULL");
+  if (n_coef < 0 || n_out < 1 || (n_coef && (!node_ids || !c_re)))
+    return fail(ACEDAG_EINVAL, "bad coefficient arguments");
+  DevGuard dg(P->device);
+  try {
+    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, 32, P->host);
+  } catch (const std::domain_error& e) {
+    return fail(ACEDAG_ENOTTARGET, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ACEDAG_ENOMEM, "out of host memory compiling the plan");
+  } catch (const std::exception& e) {
+    return fail(ACEDAG_EINVAL, e.what());
+  }
+  const PlanHost& H = P->host;
+  if (H.max_order > 6) return fail(ACEDAG_EUNSUPPORTED, "device programs support order <= 6");
+  P->U = (int)H.slot_label.size();
+  std::vector<uint16_t> ident(P->U);
+  std::vector<int32_t> used(P->U);
+  for (int i = 0; i < P->U; ++i) { ident[i] = (uint16_t)i; used[i] = H.slot_label[i]; }
+  CK(P->slot_label.upload(H.slot_label));
+  CK(P->slot_identity.upload(ident));
+  CK(P->used_labels.upload(used));
+  CK(P->ops.upload(H.ops));
+  CK(P->chunk.upload(H.chunk));
+  CK(P->cre.upload(H.cre));
+  CK(P->cim.upload(H.cim));
+  CK(P->nseg.upload(H.naive_seg));
+  CK(P->nslots.upload(H.naive_slots));
+  CK(P->ncre.upload(H.naive_cre));
+  CK(P->ncim.upload(H.naive_cim));
+  P->has_coef = true;
+  return ACEDAG_OK;
+}
+
+int acedag_plan_program(const acedag_graph* h, const int64_t* node_ids, const double* c_re,
+                        const double* c_im, int64_t n_coef, int32_t n_out, int32_t warps,
+                        uint16_t* slot_label, int64_t* n_slots, void* ops, int64_t* n_ops,
+                        int32_t* chunk, int64_t* stats) {
+  if (!h || !n_slots || !n_ops || warps < 1 || n_out < 1 || (n_coef && (!node_ids || !c_re)))
+    return fail(ACEDAG_EINVAL, "bad arguments");
+  PlanHost H;
+  try {
+    compile_plan(h->g, node_ids, c_re, c_im, n_coef, n_out, warps, H);
+  } catch (const std::domain_error& e) {
+    return fail(ACEDAG_ENOTTARGET, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ACEDAG_ENOMEM, "out of host memory compiling the plan");
+  } catch (const std::exception& e) {
+    return fail(ACEDAG_EINVAL, e.what());
+  }
+  if (slot_label) std::memcpy(slot_label, H.slot_label.data(), H.slot_label.size() * sizeof(uint16_t));
+  if (ops) std::memcpy(ops, H.ops.data(), H.ops.size() * sizeof(Op));
+  if (chunk) std::memcpy(chunk, H.chunk.data(), H.chunk.size() * sizeof(int32_t));
+  if (stats) {
+    stats[0] = H.recursive_products;
+    stats[1] = H.extra_nodes;
+    stats[2] = H.naive_products;
+  }
+  *n_slots = (int64_t)H.slot_label.size();
+  *n_ops = (int64_t)H.ops.size();
+  return ACEDAG_OK;
+}
+
+int acedag_plan_info(const acedag_plan* P, int64_t* recursive_products, int64_t* extra_nodes,
+                     int64_t* naive_products, int64_t* used_seeds) {
+  if (!P) return fail(ACEDAG_EINVAL, "plan is NULL");
+  if (!P->has_coef) return fail(ACEDAG_EINVAL, "plan has no coefficients");
+  if (recursive_products) *recursive_products = P->host.recursive_products;
+  if (extra_nodes) *extra_nodes = P->host.extra_nodes;
+  if (naive_products) *naive_products = P->host.naive_products;
+  if (used_seeds) *used_seeds = P->U;
+  return ACEDAG_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ dispatch
+namespace {
+
+constexpr int kWarps = 32;
+constexpr int kNC = 8;
+
+struct Launch {
+  int grid, block, us;
+  size_t smem;
+  bool hyb;
+};
+
+// tile geometry: 32 sites per CTA, seeds [Us][32] in smem, the rest in gcache
+int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, Launch& lc) {
+  const int64_t ntiles = (S + 31) / 32;
+  lc.block = kWarps * 32;
+  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
+  size_t avail = P->smem_optin > red_bytes ? P->smem_optin - red_bytes : 0;
+  int us_max = (int)(avail / (32 * elem));
+  lc.us = std::min(P->U, us_max);
+  lc.hyb = lc.us < P->U;
+  lc.smem = (size_t)lc.us * 32 * elem + red_bytes;
+  if (lc.hyb) {
+    size_t need = (size_t)lc.grid * (P->U - lc.us) * 32 * (elem == 16 ? 1 : 1);
+    // gcache is sized in double2 units; float2 entries use half of each slot
+    if (P->gcache.alloc(need) != cudaSuccess) return fail(ACEDAG_ENOMEM, "gcache allocation failed");
+  }
+  return 0;
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t smem) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int NU, typename T, bool HYB>
+cudaError_t launch_fast(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
+                        double* out, const Launch& lc, cudaStream_t st) {
+  auto k = dev::k2_fast<NU, T, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  k<<<lc.grid, lc.block, lc.smem, st>>>(
+      reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
+      P->chunk.p, out, reinterpret_cast<typename dev::V2<T>::t*>(P->gcache.p));
+  return cudaGetLastError();
+}
+
+template <int NU, bool HYB>
+cudaError_t launch_general(acedag_plan* P, const double2* A, int64_t S, int L,
+                           const uint16_t* slot_label, int complex_out, void* out, const Launch& lc,
+                           cudaStream_t st) {
+  auto k = dev::k2_general<NU, kNC, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  for (int o0 = 0; o0 < P->host.n_out; o0 += kNC) {
+    k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p,
+                                          P->cre.p, P->host.complex_coef ? P->cim.p : nullptr,
+                                          P->host.n_out, o0, complex_out, out, P->gcache.p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <int NU, bool GEN, bool HYB>
+cudaError_t launch_naive(acedag_plan* P, const double2* A, int64_t S, int L,
+                         const uint16_t* slot_label, int complex_out, void* out, const Launch& lc,
+                         cudaStream_t st) {
+  auto k = dev::k3_naive<NU, GEN, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  for (int o0 = 0; o0 < P->host.n_out; ++o0) {
+    k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->nseg.p, P->nslots.p,
+                                          P->ncre.p, P->host.complex_coef ? P->ncim.p : nullptr,
+                                          P->host.n_out, o0, complex_out, out, P->gcache.p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// runtime NU -> template
+template <template <int> class F, typename... Args>
+cudaError_t by_order(int nu, Args&&... a) {
+  switch (nu) {
+    case 2: return F<2>::run(a...);
+    case 3: return F<3>::run(a...);
+    case 4: return F<4>::run(a...);
+    case 5: return F<5>::run(a...);
+    case 6: return F<6>::run(a...);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int NU> struct FastF64 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_fast<NU, double, true>(a...) : launch_fast<NU, double, false>(a...);
+  }
+};
+template <int NU> struct FastF32 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_fast<NU, float, true>(a...) : launch_fast<NU, float, false>(a...);
+  }
+};
+template <int NU> struct General {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_general<NU, true>(a...) : launch_general<NU, false>(a...);
+  }
+};
+template <int NU> struct NaiveFast {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_naive<NU, false, true>(a...) : launch_naive<NU, false, false>(a...);
+  }
+};
+template <int NU> struct NaiveGen {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_naive<NU, true, true>(a...) : launch_naive<NU, true, false>(a...);
+  }
+};
+
+int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A, int64_t S, int L,
+              const uint16_t* slot_label, void* out, cudaStream_t st) {
+  const PlanHost& H = P->host;
+  const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
+  Launch lc;
+  cudaError_t e;
+  if (method == ACEDAG_METHOD_RECURSIVE) {
+    if (prec == ACEDAG_PREC_F32) {
+      if (!fast) return fail(ACEDAG_EUNSUPPORTED, "fp32 mode supports real coefficients, one real output");
+      int rc = plan_launch(P, S, sizeof(float2), kWarps * 32 * sizeof(double), lc);
+      if (rc) return rc;
+      e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+    } else if (fast) {
+      int rc = plan_launch(P, S, sizeof(double2), kWarps * 32 * sizeof(double), lc);
+      if (rc) return rc;
+      e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+    } else {
+      int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), lc);
+      if (rc) return rc;
+      e = by_order<General>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label,
+                            out_kind == ACEDAG_OUT_COMPLEX ? 1 : 0, out, lc, st);
+    }
+  } else {
+    if (prec != ACEDAG_PREC_F64) return fail(ACEDAG_EUNSUPPORTED, "naive path is fp64 only");
+    int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), lc);
+    if (rc) return rc;
+    const int nu = std::max(2, H.naive_max_order);
+    if (fast) e = by_order<NaiveFast>(nu, lc.hyb, P, (const double2*)A, S, L, slot_label, 0, out, lc, st);
+    else
+      e = by_order<NaiveGen>(nu, lc.hyb, P, (const double2*)A, S, L, slot_label,
+                             out_kind == ACEDAG_OUT_COMPLEX ? 1 : 0, out, lc, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return ACEDAG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int acedag_eval(const acedag_plan* Pc, int method, int prec, int out_kind, const void* A, int64_t S,
+                void* out, void* stream) {
+  acedag_plan* P = const_cast<acedag_plan*>(Pc);
+  if (!P || !out || (S > 0 && !A)) return fail(ACEDAG_EINVAL, "NULL argument");
+  if (!P->has_coef) return fail(ACEDAG_EINVAL, "plan has no coefficients (acedag_plan_set_coefficients)");
+  if (method != ACEDAG_METHOD_RECURSIVE && method != ACEDAG_METHOD_NAIVE)
+    return fail(ACEDAG_EINVAL, "unknown method");
+  if (prec != ACEDAG_PREC_F64 && prec != ACEDAG_PREC_F32) return fail(ACEDAG_EINVAL, "unknown precision");
+  if (out_kind != ACEDAG_OUT_REAL && out_kind != ACEDAG_OUT_COMPLEX)
+    return fail(ACEDAG_EINVAL, "unknown output kind");
+  if (S < 0) return fail(ACEDAG_EINVAL, "negative site count");
+  if (S == 0) return ACEDAG_OK;
+  DevGuard dg(P->device);
+  return eval_impl(P, method, prec, out_kind, A, S, (int)P->g->n_seeds(), P->slot_label.p, out,
+                   (cudaStream_t)stream);
+}
+
+int acedag_reduce_sites(const acedag_plan* P, const double* phi, int64_t S, double* out_total,
+                        void* stream) {
+  if (!P || !out_total || (S > 0 && !phi)) return fail(ACEDAG_EINVAL, "NULL argument");
+  if (!P->has_coef) return fail(ACEDAG_EINVAL, "plan has no coefficients");
+  DevGuard dg(P->device);
+  dev::k_reduce_sites<<<P->host.n_out, 1024, 0, (cudaStream_t)stream>>>(phi, S, P->host.n_out, out_total);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_reduce_sites");
+  return ACEDAG_OK;
+}
+
+int acedag_naive_products(const double* vals, const int32_t* lens, int64_t n, int32_t width,
+                          double* out, void* stream) {
+  if (n < 0 || width < 0 || !out || (n > 0 && width > 0 && !vals)) return fail(ACEDAG_EINVAL, "bad arguments");
+  if (n == 0) return ACEDAG_OK;
+  int grid = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
+  dev::k_naive_products<<<grid, 128, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const double2*>(vals), lens, n, width, reinterpret_cast<double2*>(out));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_naive_products");
+  return ACEDAG_OK;
+}
+
+int acedag_eval_nodes(const acedag_plan* P, const double* A, int64_t S, double* node_vals, void* stream) {
+  if (!P || !node_vals || (S > 0 && !A)) return fail(ACEDAG_EINVAL, "NULL argument");
+  if (S <= 0) return S < 0 ? fail(ACEDAG_EINVAL, "negative site count") : ACEDAG_OK;
+  DevGuard dg(P->device);
+  const int64_t N = (int64_t)P->g->tuples.size();
+  const int L = (int)P->g->n_seeds();
+  int grid = (int)std::min<int64_t>((S + 127) / 128, (int64_t)P->sms * 16);
+  dev::k_eval_nodes<<<grid, 128, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const double2*>(A), S, L, N, P->pa.p, P->pb.p, reinterpret_cast<double2*>(node_vals));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_eval_nodes");
+  return ACEDAG_OK;
+}
+
+int acedag_check_coords(int group, const double* c, int64_t n) {
+  static const int nc[4] = {1, 2, 3, 4};
+  if (group < 0 || group > 3) return fail(ACEDAG_EINVAL, "unknown group");
+  if (n > 0 && !c) return fail(ACEDAG_EINVAL, "NULL coordinates");
+  for (int64_t i = 0; i < n; ++i) {
+    const double* p = c + i * nc[group];
+    char buf[96];
+    if (group != kT && !(p[0] >= 0.0 && p[0] <= 1.0)) {
+      snprintf(buf, sizeof buf, "%.17g", p[0]);
+      return fail(ACEDAG_EDOMAIN, std::string("radius must lie in [0, 1], got ") + buf);
+    }
+    if (group == kO3F && !(p[3] >= -1.0 && p[3] <= 1.0)) {
+      snprintf(buf, sizeof buf, "%.17g", p[3]);
+      return fail(ACEDAG_EDOMAIN, std::string("feature value must lie in [-1, 1], got ") + buf);
+    }
+  }
+  return ACEDAG_OK;
+}
+
+int acedag_pool(int group, int cap, const double* coords, const int32_t* counts, int64_t S, int32_t J,
+                double* A_out, void* stream) {
+  if (group < 0 || group > 3) return fail(ACEDAG_EINVAL, "unknown group");
+  if (cap < 0 || S < 0 || J < 0 || !A_out || (S > 0 && J > 0 && !coords))
+    return fail(ACEDAG_EINVAL, "bad pool arguments");
+  if ((group == kO3 || group == kO3F) && cap > ACEDAG_YLM_LMAX)
+    return fail(ACEDAG_EUNSUPPORTED, "degree cap above the compiled Y_lm table");
+  const int dev = current_device();
+  int rc = ensure_norms(dev);
+  if (rc) return rc;
+  const int4* labels = nullptr;
+  rc = device_labels(dev, group, cap, &labels);
+  if (rc) return rc;
+  const int L = (int)one_particle_indices(group, cap).size();
+  const int64_t total = S * (int64_t)L;
+  if (total == 0) return ACEDAG_OK;
+  int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 64);
+  cudaStream_t st = (cudaStream_t)stream;
+  double2* out = reinterpret_cast<double2*>(A_out);
+  switch (group) {
+    case 0: dev::pool_ref<0><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); break;
+    case 1: dev::pool_ref<1><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); break;
+    case 2: dev::pool_ref<2><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); break;
+    default: dev::pool_ref<3><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pool_ref");
+  return ACEDAG_OK;
+}
+
+static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts, int64_t S, int J,
+                               double r_in, double r_cut, const int32_t* out_labels, int L_out,
+                               int64_t out_stride, double* A_out, cudaStream_t st) {
+  if (cap < 0 || cap > ACEDAG_YLM_LMAX) return fail(ACEDAG_EUNSUPPORTED, "degree cap outside [0, 40]");
+  if (!(r_cut > r_in) || !(r_in >= 0.0)) return fail(ACEDAG_EINVAL, "need 0 <= r_in < r_cut");
+  const int dev = current_device();
+  int rc = ensure_norms(dev);
+  if (rc) return rc;
+  const int4* labels = nullptr;
+  rc = device_labels(dev, kO3, cap, &labels);
+  if (rc) return rc;
+  const int L = (int)one_particle_indices(kO3, cap).size();
+  if (S == 0) return ACEDAG_OK;
+  const size_t smem = (size_t)std::max(J, 1) * dev::pos_stride(cap) * sizeof(double);
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (smem > (size_t)optin) return fail(ACEDAG_EUNSUPPORTED, "too many neighbours per site for the pool tables");
+  CK(cudaFuncSetAttribute(dev::pool_positions, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int grid = (int)std::min<int64_t>(S, 148 * 8);
+  dev::pool_positions<<<grid, 128, smem, st>>>(xyz, counts, S, J, cap, r_in, r_cut, labels, L,
+                                               out_labels, out_labels ? L_out : L,
+                                               out_labels ? out_stride : L,
+                                               reinterpret_cast<double2*>(A_out));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pool_positions");
+  return ACEDAG_OK;
+}
+
+int acedag_pool_positions(int cap, const double* xyz, const int32_t* counts, int64_t S, int32_t J,
+                          double r_in, double r_cut, double* A_out, void* stream) {
+  if (S < 0 || J < 0 || !A_out || (S > 0 && J > 0 && !xyz)) return fail(ACEDAG_EINVAL, "bad pool arguments");
+  return pool_positions_impl(cap, xyz, counts, S, J, r_in, r_cut, nullptr, 0, 0, A_out,
+                             (cudaStream_t)stream);
+}
+
+int acedag_eval_from_positions(acedag_plan* P, const double* xyz, const int32_t* counts, int64_t S,
+                               int32_t J, double r_in, double r_cut, int out_kind, void* out,
+                               void* stream) {
+  if (!P || !out || S < 0 || J < 0 || (S > 0 && J > 0 && !xyz)) return fail(ACEDAG_EINVAL, "bad arguments");
+  if (!P->has_coef) return fail(ACEDAG_EINVAL, "plan has no coefficients");
+  if (P->g->group != kO3) return fail(ACEDAG_EUNSUPPORTED, "positions input needs an O3 graph");
+  if (S == 0) return ACEDAG_OK;
+  DevGuard dg(P->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t chunk = 1 << 17;
+  const int U = P->U;
+  if (P->ws_A.alloc((size_t)std::min<int64_t>(S, chunk) * U) != cudaSuccess)
+    return fail(ACEDAG_ENOMEM, "workspace allocation failed");
+  const int cap = P->g->spec.int_cap();
+  const size_t osz = out_kind == ACEDAG_OUT_COMPLEX ? 16 : 8;
+  for (int64_t s0 = 0; s0 < S; s0 += chunk) {
+    const int64_t n = std::min(chunk, S - s0);
+    int rc = pool_positions_impl(cap, xyz + s0 * J * 3, counts ? counts + s0 : nullptr, n, J, r_in, r_cut,
+                                 P->used_labels.p, U, U, reinterpret_cast<double*>(P->ws_A.p), st);
+    if (rc) return rc;
+    rc = eval_impl(P, ACEDAG_METHOD_RECURSIVE, ACEDAG_PREC_F64, out_kind, P->ws_A.p, n, U,
+                   P->slot_identity.p, static_cast<char*>(out) + s0 * P->host.n_out * osz, st);
+    if (rc) return rc;
+  }
+  return ACEDAG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,203 @@
+// K1: the atomic basis (pool).
+//
+// pool_ref<GROUP>: the reference convention (evaluator.py:61-90) for all four
+// groups, one thread per (site, label), particles summed in order from 0j.
+// Recurrences use explicit round-to-nearest intrinsics so the compiler does
+// not contract them into FMAs: chebyshev (special.py:19-28), the upward-l
+// associated Legendre recursion with Condon-Shortley phase (special.py:31-47)
+// and the exact-factorial norm table (special.py:57-59, ylm_norms.h).  Only
+// cos/sin may differ from the host libm by an ulp.
+//
+// pool_positions: BASELINE cfg3/cfg5 -- Cartesian neighbour vectors, one CTA
+// per site: per-neighbour radial/Legendre/phase tables are built once in
+// shared memory, then every label is a J-term dot product.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ylm_norms.h"
+
+namespace acedag {
+namespace dev {
+
+__constant__ double c_ylm_norm[(ACEDAG_YLM_LMAX + 1) * (ACEDAG_YLM_LMAX + 2) / 2];
+
+__device__ __forceinline__ double cheb_exact(int k, double x) {  // special.py:19-28
+  if (k == 0) return 1.0;
+  double prev = 1.0, cur = x;
+  const double two_x = __dmul_rn(2.0, x);
+  for (int i = 0; i < k - 1; ++i) {
+    double nxt = __dsub_rn(__dmul_rn(two_x, cur), prev);
+    prev = cur;
+    cur = nxt;
+  }
+  return cur;
+}
+
+__device__ __forceinline__ double legendre_exact(int l, int m, double x) {  // special.py:31-47
+  const double sx = __dsqrt_rn(fmax(0.0, __dmul_rn(__dsub_rn(1.0, x), __dadd_rn(1.0, x))));
+  double pmm = 1.0;
+  for (int k = 1; k <= m; ++k) pmm = __dmul_rn(pmm, __dmul_rn((double)(-(2 * k - 1)), sx));
+  if (l == m) return pmm;
+  double pm1 = __dmul_rn(__dmul_rn(x, (double)(2 * m + 1)), pmm);
+  if (l == m + 1) return pm1;
+  for (int ll = m + 2; ll <= l; ++ll) {
+    double t = __dsub_rn(__dmul_rn(__dmul_rn(x, (double)(2 * ll - 1)), pm1),
+                         __dmul_rn((double)(ll + m - 1), pmm));
+    pmm = pm1;
+    pm1 = __ddiv_rn(t, (double)(ll - m));
+  }
+  return pm1;
+}
+
+// Y_l^m(theta, phi) as the reference computes it (special.py:50-63)
+__device__ __forceinline__ double2 sph_harm_exact(int l, int m, double theta, double phi) {
+  const int am = m < 0 ? -m : m;
+  const double np = __dmul_rn(c_ylm_norm[l * (l + 1) / 2 + am], legendre_exact(l, am, cos(theta)));
+  double sn, cs;
+  sincos(__dmul_rn((double)am, phi), &sn, &cs);
+  double2 y = make_double2(__dmul_rn(np, cs), __dmul_rn(np, sn));
+  if (m < 0) {
+    const double sg = (am & 1) ? -1.0 : 1.0;
+    y = make_double2(__dmul_rn(sg, y.x), -__dmul_rn(sg, y.y));
+  }
+  return y;
+}
+
+// labels: int4 (n, l, m, f) per label, or (m,0,0,0) for T and (n,m,0,0) for SO2
+template <int GROUP>
+__global__ void pool_ref(const double* __restrict__ coords, const int32_t* __restrict__ counts,
+                         int64_t S, int J, const int4* __restrict__ labels, int L,
+                         double2* __restrict__ out) {
+  constexpr int NC = GROUP == 0 ? 1 : (GROUP == 1 ? 2 : (GROUP == 2 ? 3 : 4));
+  const int64_t total = S * (int64_t)L;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = idx / L;
+    const int4 e = labels[idx - s * L];
+    const int nj = counts ? counts[s] : J;
+    double ar = 0.0, ai = 0.0;
+    for (int j = 0; j < nj; ++j) {
+      const double* c = coords + (s * J + j) * NC;
+      double vr, vi;
+      if (GROUP == 0) {  // e^{i m theta}
+        double sn, cs;
+        sincos(__dmul_rn((double)e.x, c[0]), &sn, &cs);
+        vr = cs;
+        vi = sn;
+      } else if (GROUP == 1) {  // R_n(r) e^{-i m theta}
+        const double R = cheb_exact(e.x, __dsub_rn(__dmul_rn(2.0, c[0]), 1.0));
+        double sn, cs;
+        sincos(__dmul_rn((double)(-e.y), c[1]), &sn, &cs);
+        vr = __dmul_rn(R, cs);
+        vi = __dmul_rn(R, sn);
+      } else {  // R_n(r) Y_l^m [T_f(mu)]
+        const double R = cheb_exact(e.x, __dsub_rn(__dmul_rn(2.0, c[0]), 1.0));
+        const double2 y = sph_harm_exact(e.y, e.z, c[1], c[2]);
+        vr = __dmul_rn(R, y.x);
+        vi = __dmul_rn(R, y.y);
+        if (GROUP == 3) {
+          const double tf = cheb_exact(e.w, c[3]);
+          vr = __dmul_rn(vr, tf);
+          vi = __dmul_rn(vi, tf);
+        }
+      }
+      ar = __dadd_rn(ar, vr);
+      ai = __dadd_rn(ai, vi);
+    }
+    out[idx] = make_double2(ar, ai);
+  }
+}
+
+// ------------------------------------------------------------ positions
+// Per-neighbour table layout in smem (doubles): w | R[0..cap] | cos m phi,
+// sin m phi [0..cap] | Pbar[l(l+1)/2 + m] for l <= cap.
+__host__ __device__ inline int pos_stride(int cap) {
+  return 1 + (cap + 1) + 2 * (cap + 1) + (cap + 1) * (cap + 2) / 2;
+}
+
+__global__ void pool_positions(const double* __restrict__ xyz, const int32_t* __restrict__ counts,
+                               int64_t S, int J, int cap, double r_in, double r_cut,
+                               const int4* __restrict__ labels, int L,
+                               const int32_t* __restrict__ out_labels, int L_out, int64_t out_stride,
+                               double2* __restrict__ out) {
+  extern __shared__ double tabs[];
+  const int st = pos_stride(cap);
+  const double inv_span = 1.0 / (r_cut - r_in);
+  for (int64_t s = blockIdx.x; s < S; s += gridDim.x) {
+    const int nj = counts ? min(counts[s], J) : J;
+    for (int j = threadIdx.x; j < nj; j += blockDim.x) {
+      double* t = tabs + j * st;
+      const double* p = xyz + (s * J + j) * 3;
+      const double x = p[0], y = p[1], z = p[2];
+      const double rho2 = x * x + y * y;
+      const double r = sqrt(rho2 + z * z);
+      const double w = r < r_cut ? 0.5 * (1.0 + cospi(r / r_cut)) : 0.0;
+      t[0] = w;
+      // radial: T_n(2 xs - 1), xs = (r - r_in)/(r_cut - r_in) clamped
+      const double xs = fmin(1.0, fmax(0.0, (r - r_in) * inv_span));
+      const double u = 2.0 * xs - 1.0;
+      double* R = t + 1;
+      R[0] = 1.0;
+      if (cap >= 1) R[1] = u;
+      for (int n = 2; n <= cap; ++n) R[n] = 2.0 * u * R[n - 1] - R[n - 2];
+      // azimuthal phase e^{i m phi} by complex powers of (x + i y)/rho
+      double* E = R + (cap + 1);
+      const double rho = sqrt(rho2);
+      double ec = 1.0, es = 0.0;
+      if (rho > 0.0) { ec = x / rho; es = y / rho; }
+      double pc = 1.0, ps = 0.0;
+      for (int m = 0; m <= cap; ++m) {
+        E[2 * m] = pc;
+        E[2 * m + 1] = ps;
+        const double nc = pc * ec - ps * es;
+        ps = pc * es + ps * ec;
+        pc = nc;
+      }
+      // normalised associated Legendre, ct = cos theta, stt = sin theta
+      double* Pb = E + 2 * (cap + 1);
+      const double ct = r > 0.0 ? z / r : 1.0;
+      const double stt = r > 0.0 ? rho / r : 0.0;
+      double pmm = 1.0;
+      for (int m = 0; m <= cap; ++m) {
+        if (m > 0) pmm *= -(2.0 * m - 1.0) * stt;
+        double p0 = pmm;
+        Pb[m * (m + 1) / 2 + m] = c_ylm_norm[m * (m + 1) / 2 + m] * p0;
+        if (m + 1 <= cap) {
+          double p1 = ct * (2.0 * m + 1.0) * p0;
+          Pb[(m + 1) * (m + 2) / 2 + m] = c_ylm_norm[(m + 1) * (m + 2) / 2 + m] * p1;
+          for (int l = m + 2; l <= cap; ++l) {
+            const double p2 = (ct * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) / (double)(l - m);
+            Pb[l * (l + 1) / 2 + m] = c_ylm_norm[l * (l + 1) / 2 + m] * p2;
+            p0 = p1;
+            p1 = p2;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < L_out; k += blockDim.x) {
+      const int lab = out_labels ? out_labels[k] : k;
+      const int4 e = labels[lab];  // (n, l, m, 0)
+      const int am = e.z < 0 ? -e.z : e.z;
+      const int pidx = 1 + (cap + 1) + 2 * (cap + 1) + e.y * (e.y + 1) / 2 + am;
+      double ar = 0.0, ai = 0.0;
+      for (int j = 0; j < nj; ++j) {
+        const double* t = tabs + j * st;
+        const double a = t[0] * t[1 + e.x] * t[pidx];
+        ar += a * t[1 + (cap + 1) + 2 * am];
+        ai += a * t[1 + (cap + 1) + 2 * am + 1];
+      }
+      if (e.z < 0) {  // Y_l^{-m} = (-1)^m conj(Y_l^m)
+        const double sg = (am & 1) ? -1.0 : 1.0;
+        ar = sg * ar;
+        ai = -sg * ai;
+      }
+      out[s * out_stride + k] = make_double2(ar, ai);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace dev
+}  // namespace acedag

@@ -1,0 +1,227 @@
+"""CUDA path vs the oracle / the reference's golden vectors, through the C ABI.
+
+Gates:
+  * node values (acedag_eval_nodes): bit-identical to evaluate_graph;
+  * fp64 phi: |phi_gpu - phi_ref| <= 1e-11 * sum_k |c_k Re A_k| per site;
+  * fp32 mode: same normalisation with 1e-5;
+  * naive_eval rows: bit-identical.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2202_04140_b200 as P
+from _helpers import phi_gate, seeded_A
+from oracle import acedag_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_phi(g, A, ids, c):
+    re, im = O.evaluate_nodes(g.parents[:, 0], g.parents[:, 1], A)
+    pr, pi = O.model_sum(re, im, ids, c)
+    return pr, pi, O.energy_scale(re, ids, c)
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    return P.build_graph(P.Group.O3, P.DegreeSpec(1, 8), 3)
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    return P.build_graph(P.Group.O3, P.DegreeSpec(1, 12), 4)
+
+
+def test_eval_nodes_bit_exact_vs_reference_cfg1(cuda, golden, cfg1):
+    d = golden("eval_cfg1.npz")
+    A = torch.from_numpy(d["A"]).to(cuda)
+    vals = cfg1.plan().evaluate_nodes(A).cpu().numpy()
+    assert np.array_equal(vals.view(np.float64), d["node_values"].view(np.float64))
+
+
+@pytest.mark.parametrize("method", ["recursive", "naive"])
+def test_phi_vs_reference_golden_cfg1(cuda, golden, cfg1, method):
+    d = golden("eval_cfg1.npz")
+    plan = P.SitePlan(cfg1).set_coefficients(node_ids=d["target_ids"], values=d["coef"])
+    phi = plan.evaluate(torch.from_numpy(d["A"]).to(cuda), method=method).cpu().numpy()
+    re, im = O.evaluate_nodes(cfg1.parents[:, 0], cfg1.parents[:, 1], d["A"])
+    ok, worst = phi_gate(phi, d["phi"].real, O.energy_scale(re, d["target_ids"], d["coef"]))
+    assert ok, worst
+
+
+@pytest.mark.parametrize("method", ["recursive", "naive"])
+def test_phi_vs_reference_golden_cfg2(cuda, golden, cfg2, method):
+    d = golden("eval_cfg2.npz")
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=d["target_ids"], values=d["coef"])
+    phi = plan.evaluate(torch.from_numpy(d["A"]).to(cuda), method=method).cpu().numpy()
+    ok, worst = phi_gate(phi, d["phi"].real, d["scale"])
+    assert ok, worst
+
+
+def test_phi_cfg2_subsample_vs_oracle(cuda, cfg2):
+    S = 96
+    A = seeded_A(S, cfg2.num_seeds, 5)
+    c = np.random.default_rng(6).normal(size=len(cfg2.target_ids))
+    pr, _, scale = _oracle_phi(cfg2, A, cfg2.target_ids, c)
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
+    At = torch.from_numpy(A).to(cuda)
+    for method in ("recursive", "naive"):
+        ok, worst = phi_gate(plan.evaluate(At, method=method).cpu().numpy(), pr, scale)
+        assert ok, (method, worst)
+
+
+def test_fp32_mode_within_1e5(cuda, cfg2):
+    S = 64
+    A = seeded_A(S, cfg2.num_seeds, 8)
+    c = np.random.default_rng(9).normal(size=len(cfg2.target_ids))
+    pr, _, scale = _oracle_phi(cfg2, A, cfg2.target_ids, c)
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
+    got = plan.evaluate(torch.from_numpy(A.astype(np.complex64)).to(cuda)).cpu().numpy()
+    ok, worst = phi_gate(got, pr, scale, tol=1e-5)
+    assert ok, worst
+
+
+def test_complex_coefficients_multi_output(cuda, cfg1):
+    S, n_out = 40, 3
+    A = seeded_A(S, cfg1.num_seeds, 10)
+    rng = np.random.default_rng(11)
+    ids = cfg1.target_ids[::2]
+    C = rng.normal(size=(len(ids), n_out)) + 1j * rng.normal(size=(len(ids), n_out))
+    plan = P.SitePlan(cfg1).set_coefficients(node_ids=ids, values=C)
+    got = plan.evaluate(torch.from_numpy(A).to(cuda), out="complex").cpu().numpy()
+    gotn = plan.evaluate(torch.from_numpy(A).to(cuda), method="naive", out="complex").cpu().numpy()
+    re, im = O.evaluate_nodes(cfg1.parents[:, 0], cfg1.parents[:, 1], A)
+    for o in range(n_out):
+        pr, pi = O.model_sum(re, im, ids, C[:, o].real, C[:, o].imag)
+        scale = np.abs(C[:, o, None] * (re[ids] + 1j * im[ids])).sum(axis=0)
+        for res in (got, gotn):
+            assert phi_gate(res[:, o].real, pr, scale)[0]
+            assert phi_gate(res[:, o].imag, pi, scale)[0]
+
+
+def test_hybrid_seed_cache_cfg5_graph(cuda):
+    """D=14, nu=5 references 575 seeds: 32-site tiles overflow shared memory and
+    the cold tail of the seed table lives in the per-CTA global cache."""
+    g = P.build_graph(P.Group.O3, P.DegreeSpec(1, 14), 5)
+    S = 40
+    A = seeded_A(S, g.num_seeds, 12)
+    c = np.random.default_rng(13).normal(size=len(g.target_ids))
+    plan = P.SitePlan(g).set_coefficients(node_ids=g.target_ids, values=c)
+    assert plan.info()["used_seeds"] > 440
+    At = torch.from_numpy(A).to(cuda)
+    rec = plan.evaluate(At).cpu().numpy()
+    nai = plan.evaluate(At, method="naive").cpu().numpy()
+    pr, _, scale = _oracle_phi(g, A[:4], g.target_ids, c)
+    assert phi_gate(rec[:4], pr, scale)[0]
+    assert phi_gate(nai[:4], pr, scale)[0]
+
+
+def test_full_size_properties_cfg2(cuda, cfg2):
+    """Size-independent checks at BASELINE cfg2 size (1e5 sites): recursive ==
+    naive, determinism, z-rotation invariance (A_nlm -> e^{i m a} A_nlm leaves
+    every target invariant) and homogeneity (A -> 2A scales order o by 2^o)."""
+    S = 100_000
+    gen = torch.Generator(device=cuda).manual_seed(3)
+    A = torch.complex(torch.randn(S, cfg2.num_seeds, device=cuda, dtype=torch.float64, generator=gen),
+                      torch.randn(S, cfg2.num_seeds, device=cuda, dtype=torch.float64, generator=gen)) * math.sqrt(0.5)
+    c = np.random.default_rng(4).normal(size=len(cfg2.target_ids))
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
+    rec = plan.evaluate(A)
+    assert torch.equal(rec, plan.evaluate(A))
+    nai = plan.evaluate(A, method="naive")
+    # sum_k |c_k| prod |A| >= sum_k |c_k Re A_k|: the gate's normalisation, bounded
+    pabs = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=np.abs(c))
+    bound = 1e-11 * pabs.evaluate(A.abs().to(torch.complex128))
+    assert torch.all((rec - nai).abs() <= bound)
+    ms = torch.tensor([e[2] for e in cfg2.labels], device=cuda, dtype=torch.float64)
+    rot = A * torch.exp(1j * 0.7 * ms)
+    assert torch.all((plan.evaluate(rot) - rec).abs() <= bound)
+    # homogeneity on the order-4 terms only
+    ids4 = cfg2.target_ids[cfg2.order[cfg2.target_ids] == 4]
+    c4 = np.random.default_rng(5).normal(size=len(ids4))
+    p4 = P.SitePlan(cfg2).set_coefficients(node_ids=ids4, values=c4)
+    r1 = p4.evaluate(A[:4096])
+    r2 = p4.evaluate(2 * A[:4096])
+    assert torch.allclose(r2, 16 * r1, rtol=1e-9, atol=1e-9 * float(r1.abs().max()))
+
+
+def test_eval_nodes_exact_on_generalized_graph(cuda):
+    g = P.build_graph(P.Group.SO2, P.DegreeSpec(1, 8), 4, "gen", 2)
+    A = seeded_A(5, g.num_seeds, 14)
+    re, im = O.evaluate_nodes(g.parents[:, 0], g.parents[:, 1], A)
+    vals = g.plan().evaluate_nodes(torch.from_numpy(A).to(cuda)).cpu().numpy()
+    assert np.array_equal(vals.real, re.T) and np.array_equal(vals.imag, im.T)
+
+
+def test_naive_products_bit_exact(cuda, golden, cfg1):
+    d = golden("eval_cfg1.npz")
+    index = {e: i for i, e in enumerate(cfg1.labels)}
+    rows = [[index[e] for e in cfg1.elements_of(t)] for t in d["target_ids"]]
+    width = max(len(r) for r in rows)
+    vals = np.ones((len(rows), width), np.complex128)
+    lens = np.array([len(r) for r in rows], np.int32)
+    for i, r in enumerate(rows):
+        vals[i, : len(r)] = d["A"][0, r]
+    got = P.naive_products(torch.from_numpy(vals).to(cuda), torch.from_numpy(lens).to(cuda)).cpu().numpy()
+    assert np.array_equal(got.view(np.float64), d["naive_site0"].view(np.float64))
+
+
+@pytest.mark.parametrize("grp", ["T", "SO2", "O3", "O3F"])
+def test_pool_vs_reference_golden(cuda, golden, grp):
+    d = golden("pool_golden.npz")
+    group = P.Group(grp)
+    A = P.pool_batched(group, int(d[f"{grp}_cap"]), torch.from_numpy(d[f"{grp}_coords"]).to(cuda),
+                       torch.from_numpy(d[f"{grp}_counts"]).to(cuda)).cpu().numpy()
+    ref = d[f"{grp}_A"]
+    assert np.all(np.abs(A - ref) <= 1e-13 * (1 + np.abs(ref)))
+
+
+def test_positions_pool_vs_reference_golden(cuda, golden):
+    d = golden("positions_cfg3.npz")
+    A = P.pool_positions(int(d["cap"]), torch.from_numpy(d["xyz"]).to(cuda)).cpu().numpy()
+    ref = d["A"]
+    assert np.all(np.abs(A - ref) <= 1e-12 * (1 + np.abs(ref)))
+
+
+def test_fused_positions_eval_vs_oracle(cuda, golden, cfg2):
+    d = golden("positions_cfg3.npz")
+    c = np.random.default_rng(15).normal(size=len(cfg2.target_ids))
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
+    xyz = torch.from_numpy(d["xyz"]).to(cuda)
+    got = plan.evaluate_positions(xyz).cpu().numpy()
+    pr, _, scale = _oracle_phi(cfg2, d["A"], cfg2.target_ids, c)
+    assert phi_gate(got, pr, scale, tol=1e-10)[0]
+    # ragged neighbour counts: a site with k neighbours == the first k only
+    counts = torch.tensor([30, 7, 0], dtype=torch.int32, device=cuda)
+    rag = plan.evaluate_positions(xyz, counts).cpu().numpy()
+    assert rag[2] == plan.evaluate(torch.zeros(1, cfg2.num_seeds, dtype=torch.complex128, device=cuda)).item()
+    one = plan.evaluate_positions(xyz[1:2, :7].contiguous()).cpu().numpy()
+    assert abs(rag[1] - one[0]) <= 1e-12 * (1 + abs(one[0]))
+
+
+def test_reduce_sites_matches_sum(cuda, cfg1):
+    c = np.random.default_rng(16).normal(size=len(cfg1.target_ids))
+    plan = P.SitePlan(cfg1).set_coefficients(node_ids=cfg1.target_ids, values=c)
+    A = torch.from_numpy(seeded_A(1000, cfg1.num_seeds, 17)).to(cuda)
+    phi = plan.evaluate(A)
+    tot = plan.reduce_sites(phi)
+    assert torch.allclose(tot[0], phi.sum(), rtol=1e-12)
+
+
+def test_edge_sizes(cuda, cfg1):
+    c = np.ones(len(cfg1.target_ids))
+    plan = P.SitePlan(cfg1).set_coefficients(node_ids=cfg1.target_ids, values=c)
+    empty = torch.zeros((0, cfg1.num_seeds), dtype=torch.complex128, device=cuda)
+    assert plan.evaluate(empty).shape == (0,)
+    for S in (1, 31, 33, 32 * 148 + 5):
+        A = torch.from_numpy(seeded_A(S, cfg1.num_seeds, S)).to(cuda)
+        rec = plan.evaluate(A).cpu().numpy()
+        nai = plan.evaluate(A, method="naive").cpu().numpy()
+        pr, _, scale = _oracle_phi(cfg1, A[:3].cpu().numpy(), cfg1.target_ids, c)
+        assert phi_gate(rec[:3], pr, scale)[0] and phi_gate(nai[:3], pr, scale)[0]
+    zero = plan.evaluate(torch.zeros((3, cfg1.num_seeds), dtype=torch.complex128, device=cuda))
+    assert torch.all(zero == 0)

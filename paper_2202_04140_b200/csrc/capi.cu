@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -292,7 +293,7 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
     return fail(ACEDAG_EINVAL, "bad coefficient arguments");
   DevGuard dg(P->device);
   try {
-    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, 32, P->host);
+    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, 64, P->host);
   } catch (const std::domain_error& e) {
     return fail(ACEDAG_ENOTTARGET, e.what());
   } catch (const std::bad_alloc&) {
@@ -366,28 +367,41 @@ int acedag_plan_info(const acedag_plan* P, int64_t* recursive_products, int64_t*
 // ------------------------------------------------------------ dispatch
 namespace {
 
-constexpr int kWarps = 32;
+constexpr int kWarps = 32;  // general / naive kernels
 constexpr int kNC = 8;
 
 struct Launch {
-  int grid, block, us;
+  int grid, block, us, rows;
   size_t smem;
   bool hyb;
 };
 
-// tile geometry: 32 sites per CTA, seeds [Us][32] in smem, the rest in gcache
-int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, Launch& lc) {
+// K2 fast-path geometry: warps per CTA (16 -> 128 registers and 8-leaf
+// batches, 32 -> 64 registers and 4-leaf batches); ACEDAG_K2_WARPS overrides.
+int k2_warps() {
+  static int w = [] {
+    const char* e = getenv("ACEDAG_K2_WARPS");
+    int v = e ? atoi(e) : 16;
+    return v == 32 ? 32 : 16;
+  }();
+  return w;
+}
+
+// tile geometry: 32 sites per CTA, seed rows [Us][32] in smem (U used seeds
+// plus the constant ONE row), the tail in the per-CTA global cache
+int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, int warps, Launch& lc) {
   const int64_t ntiles = (S + 31) / 32;
-  lc.block = kWarps * 32;
+  lc.block = warps * 32;
   lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
+  lc.rows = P->U + 1;
   size_t avail = P->smem_optin > red_bytes ? P->smem_optin - red_bytes : 0;
   int us_max = (int)(avail / (32 * elem));
-  lc.us = std::min(P->U, us_max);
-  lc.hyb = lc.us < P->U;
+  lc.us = std::min(lc.rows, us_max);
+  lc.hyb = lc.us < lc.rows;
   lc.smem = (size_t)lc.us * 32 * elem + red_bytes;
   if (lc.hyb) {
-    size_t need = (size_t)lc.grid * (P->U - lc.us) * 32 * (elem == 16 ? 1 : 1);
-    // gcache is sized in double2 units; float2 entries use half of each slot
+    // sized in double2 units; float2 tables use the first half
+    size_t need = (size_t)lc.grid * (lc.rows - lc.us) * 32;
     if (P->gcache.alloc(need) != cudaSuccess) return fail(ACEDAG_ENOMEM, "gcache allocation failed");
   }
   return 0;
@@ -398,16 +412,25 @@ cudaError_t set_smem(K kernel, size_t smem) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-template <int NU, typename T, bool HYB>
-cudaError_t launch_fast(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
-                        double* out, const Launch& lc, cudaStream_t st) {
-  auto k = dev::k2_fast<NU, T, HYB>;
+int nchunks(const acedag_plan* P) { return (int)P->host.chunk.size() - 1; }
+
+template <int NU, typename T, int WARPS, int MAXU, bool HYB>
+cudaError_t launch_fast_w(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
+                          double* out, const Launch& lc, cudaStream_t st) {
+  auto k = dev::k2_fast<NU, T, WARPS, MAXU, HYB>;
   cudaError_t e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
   k<<<lc.grid, lc.block, lc.smem, st>>>(
       reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
-      P->chunk.p, out, reinterpret_cast<typename dev::V2<T>::t*>(P->gcache.p));
+      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(P->gcache.p));
   return cudaGetLastError();
+}
+
+template <int NU, typename T, bool HYB>
+cudaError_t launch_fast(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
+                        double* out, const Launch& lc, cudaStream_t st) {
+  if (lc.block == 32 * 32) return launch_fast_w<NU, T, 32, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
+  return launch_fast_w<NU, T, 16, 8, HYB>(P, A, S, L, slot_label, out, lc, st);
 }
 
 template <int NU, bool HYB>
@@ -419,8 +442,9 @@ cudaError_t launch_general(acedag_plan* P, const double2* A, int64_t S, int L,
   if (e != cudaSuccess) return e;
   for (int o0 = 0; o0 < P->host.n_out; o0 += kNC) {
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p,
-                                          P->cre.p, P->host.complex_coef ? P->cim.p : nullptr,
-                                          P->host.n_out, o0, complex_out, out, P->gcache.p);
+                                          nchunks(P), P->cre.p,
+                                          P->host.complex_coef ? P->cim.p : nullptr, P->host.n_out, o0,
+                                          complex_out, out, P->gcache.p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -492,22 +516,22 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
   if (method == ACEDAG_METHOD_RECURSIVE) {
     if (prec == ACEDAG_PREC_F32) {
       if (!fast) return fail(ACEDAG_EUNSUPPORTED, "fp32 mode supports real coefficients, one real output");
-      int rc = plan_launch(P, S, sizeof(float2), kWarps * 32 * sizeof(double), lc);
+      int rc = plan_launch(P, S, sizeof(float2), nchunks(P) * 32 * sizeof(double) + 16, k2_warps(), lc);
       if (rc) return rc;
       e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
     } else if (fast) {
-      int rc = plan_launch(P, S, sizeof(double2), kWarps * 32 * sizeof(double), lc);
+      int rc = plan_launch(P, S, sizeof(double2), nchunks(P) * 32 * sizeof(double) + 16, k2_warps(), lc);
       if (rc) return rc;
       e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
     } else {
-      int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), lc);
+      int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), kWarps, lc);
       if (rc) return rc;
       e = by_order<General>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label,
                             out_kind == ACEDAG_OUT_COMPLEX ? 1 : 0, out, lc, st);
     }
   } else {
     if (prec != ACEDAG_PREC_F64) return fail(ACEDAG_EUNSUPPORTED, "naive path is fp64 only");
-    int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), lc);
+    int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), kWarps, lc);
     if (rc) return rc;
     const int nu = std::max(2, H.naive_max_order);
     if (fast) e = by_order<NaiveFast>(nu, lc.hyb, P, (const double2*)A, S, L, slot_label, 0, out, lc, st);
@@ -526,7 +550,7 @@ extern "C" {
 int acedag_eval(const acedag_plan* Pc, int method, int prec, int out_kind, const void* A, int64_t S,
                 void* out, void* stream) {
   acedag_plan* P = const_cast<acedag_plan*>(Pc);
-  if (!P || !out || (S > 0 && !A)) return fail(ACEDAG_EINVAL, "NULL argument");
+  if (!P || ((!out || !A) && S > 0)) return fail(ACEDAG_EINVAL, "NULL argument");
   if (!P->has_coef) return fail(ACEDAG_EINVAL, "plan has no coefficients (acedag_plan_set_coefficients)");
   if (method != ACEDAG_METHOD_RECURSIVE && method != ACEDAG_METHOD_NAIVE)
     return fail(ACEDAG_EINVAL, "unknown method");
@@ -564,7 +588,7 @@ int acedag_naive_products(const double* vals, const int32_t* lens, int64_t n, in
 }
 
 int acedag_eval_nodes(const acedag_plan* P, const double* A, int64_t S, double* node_vals, void* stream) {
-  if (!P || !node_vals || (S > 0 && !A)) return fail(ACEDAG_EINVAL, "NULL argument");
+  if (!P || ((!node_vals || !A) && S > 0)) return fail(ACEDAG_EINVAL, "NULL argument");
   if (S <= 0) return S < 0 ? fail(ACEDAG_EINVAL, "negative site count") : ACEDAG_OK;
   DevGuard dg(P->device);
   const int64_t N = (int64_t)P->g->tuples.size();

@@ -40,7 +40,7 @@ __device__ __forceinline__ double2 cmul_exact(double2 a, double2 b) {
 
 struct OpR {
   double c;
-  uint32_t sa, sb, nch;
+  uint32_t off, nch, skip;
 };
 
 // 16-byte uniform record load (every lane reads the same address)
@@ -48,180 +48,263 @@ __device__ __forceinline__ OpR load_op(const Op* p) {
   int4 raw = __ldg(reinterpret_cast<const int4*>(p));
   OpR r;
   r.c = __hiloint2double(raw.y, raw.x);
-  r.sa = (uint32_t)raw.z & 0xFFFFu;
-  r.sb = (uint32_t)raw.z >> 16;
-  r.nch = (uint32_t)raw.w;
+  r.off = (uint32_t)raw.z;
+  r.nch = (uint32_t)raw.w & 0xFFFFu;
+  r.skip = (uint32_t)raw.w >> 16;
   return r;
 }
 
+// Seed rows addressed by the byte offset stored in the record (c128 layout:
+// slot * 512).  f32 tables use half the stride.  With HYB the rows past the
+// shared-memory budget live in a per-CTA global cache (L1/L2 resident).
 template <typename T, bool HYB>
-struct SeedTab {
+struct Seeds {
   using V = typename V2<T>::t;
-  const V* s;   // shared  [Us][32]
-  const V* g;   // global  [U-Us][32] (per-CTA cache of the cold tail)
+  static constexpr int kShift = sizeof(V) == 16 ? 0 : 1;
+  const char* s;   // shared base + lane * sizeof(V)
+  const char* g;   // global cache base + lane * sizeof(V) - us_bytes
+  uint32_t us_bytes;
+  __device__ __forceinline__ V operator()(uint32_t off) const {
+    const uint32_t o = off >> kShift;
+    if (!HYB || o < us_bytes) return *reinterpret_cast<const V*>(s + o);
+    return *reinterpret_cast<const V*>(g + o);
+  }
+};
+
+// slot-indexed view used by the naive kernel
+template <bool HYB>
+struct SlotTab {
+  const double2* s;
+  const double2* g;
   uint32_t us;
   int lane;
-  __device__ __forceinline__ V operator()(uint32_t slot) const {
+  __device__ __forceinline__ double2 operator()(uint32_t slot) const {
     if (!HYB || slot < us) return s[slot * 32 + lane];
     return g[(slot - us) * 32 + lane];
   }
 };
 
-// ---------------------------------------------------------------- K2 (fast)
-// real coefficients, Re(phi), one output: acc += c * Re(v)
-template <int D, int NU, typename T, bool HYB>
-__device__ __forceinline__ void k2_visit(const Op*& op, uint32_t nch, typename V2<T>::t pv,
-                                        T& acc0, T& acc1, const SeedTab<T, HYB>& tab) {
-  using V = typename V2<T>::t;
-  if constexpr (D > NU) {
-    return;
-  } else if constexpr (D == NU) {
-    // leaves of the deepest order: only the real part of the product
-    uint32_t j = 0;
-    for (; j + 4 <= nch; j += 4) {
-      OpR r0 = load_op(op), r1 = load_op(op + 1), r2 = load_op(op + 2), r3 = load_op(op + 3);
-      V s0 = tab(r0.sa), s1 = tab(r1.sa), s2 = tab(r2.sa), s3 = tab(r3.sa);
-      acc0 += (T)r0.c * (s0.x * pv.x - s0.y * pv.y);
-      acc1 += (T)r1.c * (s1.x * pv.x - s1.y * pv.y);
-      acc0 += (T)r2.c * (s2.x * pv.x - s2.y * pv.y);
-      acc1 += (T)r3.c * (s3.x * pv.x - s3.y * pv.y);
-      op += 4;
-    }
-    for (; j < nch; ++j) {
-      OpR r = load_op(op++);
-      V s = tab(r.sa);
-      acc0 += (T)r.c * (s.x * pv.x - s.y * pv.y);
-    }
-  } else {
-    for (uint32_t j = 0; j < nch; ++j) {
-      OpR r = load_op(op++);
-      V v = cmul(tab(r.sa), pv);
-      acc1 += (T)r.c * v.x;
-      if (r.nch) k2_visit<D + 1, NU, T, HYB>(op, r.nch, v, acc0, acc1, tab);
-    }
+// Stage the seeds one tile references: lane = site, rows [slot][32 sites],
+// plus the constant ONE row at slot U.  Rows past Us go to the global cache.
+template <typename V, bool HYB>
+__device__ __forceinline__ void stage_seeds(const V* __restrict__ A, int64_t S, int L, int64_t tile,
+                                            const uint16_t* __restrict__ slot_label, int U, int Us,
+                                            V* sA, V* gA, int warp, int W, int lane) {
+  const int64_t site = tile * 32 + lane;
+  const bool valid = site < S;
+  const V* row = A + (valid ? site : 0) * (int64_t)L;
+  for (int u = warp; u <= U; u += W) {
+    V v;
+    if (u == U) { v.x = 1; v.y = 0; }
+    else if (valid) v = row[__ldg(slot_label + u)];
+    else { v.x = 0; v.y = 0; }
+    if (!HYB || u < Us) sA[u * 32 + lane] = v;
+    else gA[(u - Us) * 32 + lane] = v;
   }
 }
 
-template <int NU, typename T, bool HYB>
-__global__ void __launch_bounds__(1024, 1)
+// ---------------------------------------------------------------- K2 (fast)
+// real coefficients, Re(phi), one output: acc += c * Re(v).
+// Deepest level: the leaves of one parent are loaded as a batch (all record
+// and seed loads in flight together) and only the real part is formed.
+template <int K, typename T, bool HYB>
+__device__ __forceinline__ void leaf_block(const Op* p, typename V2<T>::t pv, T& acc0, T& acc1,
+                                           const Seeds<T, HYB>& sd) {
+  using V = typename V2<T>::t;
+  OpR r[K];
+  V s[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = load_op(p + j);
+#pragma unroll
+  for (int j = 0; j < K; ++j) s[j] = sd(r[j].off);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const T t = s[j].x * pv.x - s[j].y * pv.y;
+    if (j & 1) acc1 += (T)r[j].c * t;
+    else acc0 += (T)r[j].c * t;
+  }
+}
+
+template <int MAXU, typename T, bool HYB>
+__device__ __forceinline__ void leaves(const Op* p, uint32_t n, typename V2<T>::t pv, T& acc0, T& acc1,
+                                       const Seeds<T, HYB>& sd) {
+  while (n >= MAXU) {
+    leaf_block<MAXU, T, HYB>(p, pv, acc0, acc1, sd);
+    p += MAXU;
+    n -= MAXU;
+  }
+  switch (n) {
+    case 1: leaf_block<1, T, HYB>(p, pv, acc0, acc1, sd); break;
+    case 2: leaf_block<2, T, HYB>(p, pv, acc0, acc1, sd); break;
+    case 3: leaf_block<3, T, HYB>(p, pv, acc0, acc1, sd); break;
+    case 4: if constexpr (MAXU > 4) leaf_block<4, T, HYB>(p, pv, acc0, acc1, sd); break;
+    case 5: if constexpr (MAXU > 5) leaf_block<5, T, HYB>(p, pv, acc0, acc1, sd); break;
+    case 6: if constexpr (MAXU > 6) leaf_block<6, T, HYB>(p, pv, acc0, acc1, sd); break;
+    case 7: if constexpr (MAXU > 7) leaf_block<7, T, HYB>(p, pv, acc0, acc1, sd); break;
+    default: break;
+  }
+}
+
+// Children of a node at order D-1 (values of order D).  `p` points at the
+// first child record and returns past the whole subtree.  The next sibling's
+// record is fetched before the current child's subtree is walked.
+template <int D, int NU, int MAXU, typename T, bool HYB>
+__device__ __forceinline__ const Op* k2_visit(const Op* p, uint32_t n, typename V2<T>::t pv,
+                                             T& acc0, T& acc1, const Seeds<T, HYB>& sd) {
+  using V = typename V2<T>::t;
+  if constexpr (D > NU) {
+    return p;
+  } else if constexpr (D == NU) {
+    leaves<MAXU, T, HYB>(p, n, pv, acc0, acc1, sd);
+    return p + n;
+  } else {
+    if (n == 0) return p;
+    OpR r = load_op(p);
+    for (uint32_t j = 0; j < n; ++j) {
+      const bool more = j + 1 < n;
+      const bool pf = more && r.skip != 0xFFFFu;
+      OpR rn;
+      if (pf) rn = load_op(p + 1 + r.skip);
+      const V v = cmul(sd(r.off), pv);
+      acc1 += (T)r.c * v.x;
+      p = k2_visit<D + 1, NU, MAXU, T, HYB>(p + 1, r.nch, v, acc0, acc1, sd);
+      if (more) r = pf ? rn : load_op(p);
+    }
+    return p;
+  }
+}
+
+template <int NU, typename T, int WARPS, int MAXU, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
 k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
         const uint16_t* __restrict__ slot_label, int U, int Us, const Op* __restrict__ ops,
-        const int32_t* __restrict__ chunk, double* __restrict__ out,
+        const int32_t* __restrict__ chunk, int nchunk, double* __restrict__ out,
         typename V2<T>::t* __restrict__ gcache) {
   using V = typename V2<T>::t;
   extern __shared__ __align__(16) unsigned char smem[];
   V* sA = reinterpret_cast<V*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)Us * 32 * sizeof(V));
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
-  V* gA = HYB ? gcache + (size_t)blockIdx.x * (U - Us) * 32 : nullptr;
-  SeedTab<T, HYB> tab{sA, gA, (uint32_t)Us, lane};
+  int* next = reinterpret_cast<int*>(red + (size_t)nchunk * 32);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  V* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
+  Seeds<T, HYB> sd;
+  sd.s = reinterpret_cast<const char*>(sA) + lane * sizeof(V);
+  sd.g = HYB ? reinterpret_cast<const char*>(gA) + lane * sizeof(V) - (size_t)Us * 32 * sizeof(V) : nullptr;
+  sd.us_bytes = (uint32_t)((size_t)Us * 32 * sizeof(V));
   const int64_t ntiles = (S + 31) / 32;
-  const Op* cbeg = ops + chunk[warp];
-  const Op* cend = ops + chunk[warp + 1];
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t site = tile * 32 + lane;
-    const bool valid = site < S;
-    const V* row = A + (valid ? site : 0) * (int64_t)L;
-    for (int u = warp; u < U; u += W) {
-      V v = valid ? row[slot_label[u]] : V{0, 0};
-      if (!HYB || u < Us) sA[u * 32 + lane] = v;
-      else gA[(u - Us) * 32 + lane] = v;
-    }
+    stage_seeds<V, HYB>(A, S, L, tile, slot_label, U, Us, sA, gA, warp, WARPS, lane);
+    if (threadIdx.x == 0) *next = 0;
     __syncthreads();
-    double acc = 0.0;
-    for (const Op* op = cbeg; op < cend;) {
-      T acc0 = 0, acc1 = 0;
-      OpR r = load_op(op++);
-      V a = tab(r.sa);
-      V v = (r.sb == kSingle) ? a : cmul(a, tab(r.sb));
-      acc0 += (T)r.c * v.x;
-      if (r.nch) k2_visit<3, NU, T, HYB>(op, r.nch, v, acc0, acc1, tab);
-      acc += (double)acc0 + (double)acc1;
+    while (true) {
+      int ci = 0;
+      if (lane == 0) ci = atomicAdd(next, 1);
+      ci = __shfl_sync(0xffffffffu, ci, 0);
+      if (ci >= nchunk) break;
+      double acc = 0.0;
+      const Op* p = ops + __ldg(chunk + ci);
+      const Op* end = ops + __ldg(chunk + ci + 1);
+      if (p < end) {
+        OpR r0 = load_op(p), r1 = load_op(p + 1);
+        while (true) {
+          const bool known = r0.skip != 0xFFFFu;
+          const Op* nxt = p + 2 + r0.skip;
+          OpR n0, n1;
+          if (known && nxt < end) { n0 = load_op(nxt); n1 = load_op(nxt + 1); }
+          T acc0 = 0, acc1 = 0;
+          const V v = cmul(sd(r0.off), sd(r1.off));
+          acc0 += (T)r0.c * v.x;
+          p = k2_visit<3, NU, MAXU, T, HYB>(p + 2, r0.nch, v, acc0, acc1, sd);
+          acc += (double)acc0 + (double)acc1;
+          if (p >= end) break;
+          if (known) { r0 = n0; r1 = n1; }
+          else { r0 = load_op(p); r1 = load_op(p + 1); }
+        }
+      }
+      red[ci * 32 + lane] = acc;
     }
-    red[warp * 32 + lane] = acc;
     __syncthreads();
     if (warp == 0) {
       double s = 0.0;
-      for (int w = 0; w < W; ++w) s += red[w * 32 + lane];
-      if (valid) out[site] = s;
+      for (int c = 0; c < nchunk; ++c) s += red[c * 32 + lane];
+      const int64_t site = tile * 32 + lane;
+      if (site < S) out[site] = s;
     }
   }
 }
 
 // ------------------------------------------------------------- K2 (general)
 // complex coefficients and/or complex output and/or several outputs: NC
-// complex accumulators per lane; coefficient table [n_ops, n_out].
+// complex accumulators per lane; coefficient table [n_records, n_out].
 template <int NC>
 struct AccC {
   double re[NC], im[NC];
 };
 
-template <int D, int NU, int NC, bool HYB>
-__device__ __forceinline__ void k2g_visit(const Op*& op, const Op* base, uint32_t nch, double2 pv,
-                                         AccC<NC>& acc, const SeedTab<double, HYB>& tab,
-                                         const double* cre, const double* cim, int n_out, int o0,
-                                         int nc) {
-  if constexpr (D > NU) {
-    return;
-  } else {
-    for (uint32_t j = 0; j < nch; ++j) {
-      const int64_t idx = op - base;
-      OpR r = load_op(op++);
-      double2 v = cmul(tab(r.sa), pv);
+template <int NC>
+__device__ __forceinline__ void acc_general(AccC<NC>& acc, double2 v, int64_t idx, const double* cre,
+                                            const double* cim, int n_out, int o0, int nc) {
 #pragma unroll
-      for (int q = 0; q < NC; ++q)
-        if (q < nc) {
-          double c_r = __ldg(cre + idx * n_out + o0 + q);
-          double c_i = cim ? __ldg(cim + idx * n_out + o0 + q) : 0.0;
-          acc.re[q] += c_r * v.x - c_i * v.y;
-          acc.im[q] += c_r * v.y + c_i * v.x;
-        }
-      if (r.nch) k2g_visit<D + 1, NU, NC, HYB>(op, base, r.nch, v, acc, tab, cre, cim, n_out, o0, nc);
+  for (int q = 0; q < NC; ++q)
+    if (q < nc) {
+      const double c_r = __ldg(cre + idx * n_out + o0 + q);
+      const double c_i = cim ? __ldg(cim + idx * n_out + o0 + q) : 0.0;
+      acc.re[q] += c_r * v.x - c_i * v.y;
+      acc.im[q] += c_r * v.y + c_i * v.x;
     }
+}
+
+template <int D, int NU, int NC, bool HYB>
+__device__ __forceinline__ const Op* k2g_visit(const Op* p, const Op* base, uint32_t n, double2 pv,
+                                              AccC<NC>& acc, const Seeds<double, HYB>& sd,
+                                              const double* cre, const double* cim, int n_out, int o0,
+                                              int nc) {
+  if constexpr (D > NU) {
+    return p;
+  } else {
+    for (uint32_t j = 0; j < n; ++j) {
+      OpR r = load_op(p);
+      const double2 v = cmul(sd(r.off), pv);
+      acc_general<NC>(acc, v, p - base, cre, cim, n_out, o0, nc);
+      p = k2g_visit<D + 1, NU, NC, HYB>(p + 1, base, r.nch, v, acc, sd, cre, cim, n_out, o0, nc);
+    }
+    return p;
   }
 }
 
 template <int NU, int NC, bool HYB>
 __global__ void __launch_bounds__(1024, 1)
 k2_general(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label,
-           int U, int Us, const Op* __restrict__ ops, const int32_t* __restrict__ chunk,
+           int U, int Us, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
            const double* __restrict__ cre, const double* __restrict__ cim, int n_out, int o0,
            int complex_out, void* __restrict__ out, double2* __restrict__ gcache) {
   extern __shared__ __align__(16) unsigned char smem[];
   double2* sA = reinterpret_cast<double2*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)Us * 32 * sizeof(double2));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
-  double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U - Us) * 32 : nullptr;
-  SeedTab<double, HYB> tab{sA, gA, (uint32_t)Us, lane};
+  double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
+  Seeds<double, HYB> sd;
+  sd.s = reinterpret_cast<const char*>(sA) + lane * 16;
+  sd.g = HYB ? reinterpret_cast<const char*>(gA) + lane * 16 - (size_t)Us * 512 : nullptr;
+  sd.us_bytes = (uint32_t)((size_t)Us * 512);
   const int nc = min(NC, n_out - o0);
   const int64_t ntiles = (S + 31) / 32;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t site = tile * 32 + lane;
-    const bool valid = site < S;
-    const double2* row = A + (valid ? site : 0) * (int64_t)L;
-    for (int u = warp; u < U; u += W) {
-      double2 v = valid ? row[slot_label[u]] : make_double2(0, 0);
-      if (!HYB || u < Us) sA[u * 32 + lane] = v;
-      else gA[(u - Us) * 32 + lane] = v;
-    }
+    stage_seeds<double2, HYB>(A, S, L, tile, slot_label, U, Us, sA, gA, warp, W, lane);
     __syncthreads();
     AccC<NC> acc;
 #pragma unroll
     for (int q = 0; q < NC; ++q) acc.re[q] = acc.im[q] = 0.0;
-    for (const Op* op = ops + chunk[warp]; op < ops + chunk[warp + 1];) {
-      const int64_t idx = op - ops;
-      OpR r = load_op(op++);
-      double2 a = tab(r.sa);
-      double2 v = (r.sb == kSingle) ? a : cmul(a, tab(r.sb));
-#pragma unroll
-      for (int q = 0; q < NC; ++q)
-        if (q < nc) {
-          double c_r = __ldg(cre + idx * n_out + o0 + q);
-          double c_i = cim ? __ldg(cim + idx * n_out + o0 + q) : 0.0;
-          acc.re[q] += c_r * v.x - c_i * v.y;
-          acc.im[q] += c_r * v.y + c_i * v.x;
-        }
-      if (r.nch) k2g_visit<3, NU, NC, HYB>(op, ops, r.nch, v, acc, tab, cre, cim, n_out, o0, nc);
+    // static chunk assignment: warp w takes chunks w, w+W, ...
+    for (int ci = warp; ci < nchunk; ci += W) {
+      const Op* p = ops + chunk[ci];
+      const Op* end = ops + chunk[ci + 1];
+      while (p < end) {
+        OpR r0 = load_op(p), r1 = load_op(p + 1);
+        const double2 v = cmul(sd(r0.off), sd(r1.off));
+        acc_general<NC>(acc, v, p - ops, cre, cim, n_out, o0, nc);
+        p = k2g_visit<3, NU, NC, HYB>(p + 2, ops, r0.nch, v, acc, sd, cre, cim, n_out, o0, nc);
+      }
     }
     // reduce over warps, one output at a time, fixed order
     for (int q = 0; q < nc; ++q) {
@@ -234,7 +317,8 @@ k2_general(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __re
           sr += red[w * 32 + lane];
           si += red[(W + w) * 32 + lane];
         }
-        if (valid) {
+        const int64_t site = tile * 32 + lane;
+        if (site < S) {
           if (complex_out) reinterpret_cast<double2*>(out)[site * n_out + o0 + q] = make_double2(sr, si);
           else reinterpret_cast<double*>(out)[site * n_out + o0 + q] = sr;
         }
@@ -256,18 +340,13 @@ k3_naive(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
   double2* sA = reinterpret_cast<double2*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)Us * 32 * sizeof(double2));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
-  double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U - Us) * 32 : nullptr;
-  SeedTab<double, HYB> tab{sA, gA, (uint32_t)Us, lane};
+  double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
+  SlotTab<HYB> tab{sA, gA, (uint32_t)Us, lane};
   const int64_t ntiles = (S + 31) / 32;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t site = tile * 32 + lane;
     const bool valid = site < S;
-    const double2* row = A + (valid ? site : 0) * (int64_t)L;
-    for (int u = warp; u < U; u += W) {
-      double2 v = valid ? row[slot_label[u]] : make_double2(0, 0);
-      if (!HYB || u < Us) sA[u * 32 + lane] = v;
-      else gA[(u - Us) * 32 + lane] = v;
-    }
+    stage_seeds<double2, HYB>(A, S, L, tile, slot_label, U, Us, sA, gA, warp, W, lane);
     __syncthreads();
     double ar = 0.0, ai = 0.0;
 #pragma unroll

@@ -171,60 +171,81 @@ void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re, c
   for (auto& n : nodes) std::sort(n.kids.begin(), n.kids.end(), by_tuple);
   P.max_order = std::max(2, max_order);
 
-  std::vector<int64_t> root_cost(roots.size(), 0), root_ops(roots.size(), 0);
-  auto emit = [&](int32_t k, uint16_t sa, uint16_t sb) {
+  // Records (16 B): {c, byte offset of the seed row, #children, subtree size}.
+  // A root is two records (its two seeds; an order-1 term pairs its seed with
+  // the constant ONE row, slot U).  Every other record multiplies its seed
+  // into the parent value held in registers.
+  const uint32_t U = (uint32_t)lab.size();
+  auto off_of = [&](uint32_t s) { return s * kRowBytes; };
+  std::vector<int64_t> root_cost(roots.size(), 0);
+  auto emit = [&](int32_t k, uint32_t off, uint32_t nch) {
     Op op;
-    op.c = nodes[k].coef >= 0 ? rows_re[nodes[k].coef * n_out] : 0.0;
-    op.sa = sa;
-    op.sb = sb;
-    op.nch = (uint32_t)nodes[k].kids.size();
+    op.c = (k >= 0 && nodes[k].coef >= 0) ? rows_re[nodes[k].coef * n_out] : 0.0;
+    op.off = off;
+    if (nch > 0xFFFFu) throw std::invalid_argument("node with more than 65535 children");
+    op.nch = (uint16_t)nch;
+    op.skip = 0;
     P.ops.push_back(op);
     for (int o = 0; o < n_out; ++o) {
-      P.cre.push_back(nodes[k].coef >= 0 ? rows_re[nodes[k].coef * n_out + o] : 0.0);
-      if (c_im) P.cim.push_back(nodes[k].coef >= 0 ? rows_im[nodes[k].coef * n_out + o] : 0.0);
+      const bool has = k >= 0 && nodes[k].coef >= 0;
+      P.cre.push_back(has ? rows_re[nodes[k].coef * n_out + o] : 0.0);
+      if (c_im) P.cim.push_back(has ? rows_im[nodes[k].coef * n_out + o] : 0.0);
     }
   };
-  std::vector<int32_t> stack;
-  // cost model in FP64 pipe slots: product 4, leaf real-part 2, coefficient 1
-  std::vector<int64_t> op_root;  // op offsets where each root starts
+  // preorder with subtree sizes patched on the way back up
+  std::vector<std::pair<int32_t, int64_t>> stack;  // (node, record index) ; node<0 = close marker
+  std::vector<int64_t> op_root;
   for (size_t r = 0; r < roots.size(); ++r) {
     int32_t k = roots[r];
     op_root.push_back((int64_t)P.ops.size());
-    int64_t cost = 0;
     if (nodes[k].t.len == 1) {
-      emit(k, slot[nodes[k].t.id[0]], kSingle);
-      cost += 2;
-    } else {
-      emit(k, slot[nodes[k].sa], slot[nodes[k].sb]);
-      cost += 6;
-      P.recursive_products++;
-      // iterative preorder over the subtree
-      stack.assign(nodes[k].kids.rbegin(), nodes[k].kids.rend());
-      while (!stack.empty()) {
-        int32_t q = stack.back();
-        stack.pop_back();
-        emit(q, slot[nodes[q].sec], 0);
-        P.recursive_products++;
-        cost += nodes[q].kids.empty() ? 4 : 6;
-        for (auto it = nodes[q].kids.rbegin(); it != nodes[q].kids.rend(); ++it) stack.push_back(*it);
-      }
+      emit(k, off_of(slot[nodes[k].t.id[0]]), 0);
+      emit(-1, off_of(U), 0);
+      root_cost[r] = 6;
+      continue;
     }
+    const int64_t r0 = (int64_t)P.ops.size();
+    emit(k, off_of(slot[nodes[k].sa]), (uint32_t)nodes[k].kids.size());
+    emit(-1, off_of(slot[nodes[k].sb]), 0);
+    P.recursive_products++;
+    int64_t cost = 8;
+    stack.clear();
+    for (auto it = nodes[k].kids.rbegin(); it != nodes[k].kids.rend(); ++it) stack.push_back({*it, -1});
+    while (!stack.empty()) {
+      auto [q, at] = stack.back();
+      stack.pop_back();
+      if (at >= 0) {  // close: subtree of record `at` ends here
+        int64_t size = (int64_t)P.ops.size() - at - 1;
+        P.ops[at].skip = size <= 0xFFFE ? (uint16_t)size : (uint16_t)0xFFFF;
+        continue;
+      }
+      const int64_t me = (int64_t)P.ops.size();
+      emit(q, off_of(slot[nodes[q].sec]), (uint32_t)nodes[q].kids.size());
+      P.recursive_products++;
+      cost += nodes[q].kids.empty() ? 4 : 6;
+      stack.push_back({q, me});
+      for (auto it = nodes[q].kids.rbegin(); it != nodes[q].kids.rend(); ++it) stack.push_back({*it, -1});
+    }
+    int64_t size = (int64_t)P.ops.size() - r0 - 2;
+    P.ops[r0].skip = size <= 0xFFFE ? (uint16_t)size : (uint16_t)0xFFFF;
     root_cost[r] = cost;
   }
-  // ---- warp chunks at root boundaries, balanced by cost
+  // ---- work chunks at root boundaries, balanced by cost (grabbed dynamically
+  // by the warps of a CTA; partial sums are combined in chunk order)
   int64_t total = 0;
   for (int64_t c : root_cost) total += c;
-  P.chunk.assign(warps + 1, (int32_t)P.ops.size());
+  const int chunks = warps;
+  P.chunk.assign(chunks + 1, (int32_t)P.ops.size());
   P.chunk[0] = 0;
   int64_t acc = 0;
   int w = 1;
-  for (size_t r = 0; r < roots.size() && w < warps; ++r) {
+  for (size_t r = 0; r < roots.size() && w < chunks; ++r) {
     acc += root_cost[r];
-    while (w < warps && acc * warps >= total * w) {
+    while (w < chunks && acc * chunks >= total * w) {
       P.chunk[w++] = (int32_t)(r + 1 < roots.size() ? op_root[r + 1] : P.ops.size());
     }
   }
-  for (; w < warps; ++w) P.chunk[w] = (int32_t)P.ops.size();
+  for (; w < chunks; ++w) P.chunk[w] = (int32_t)P.ops.size();
 
   // ---- naive program: coefficient nodes grouped by order, graph-id order
   std::vector<std::vector<int64_t>> nby(kMaxOrder + 1);

@@ -25,12 +25,13 @@ namespace acedag {
 
 // 16-byte program record, read warp-uniformly by K2.
 struct alignas(16) Op {
-  double c;      // first output's real coefficient (0 if the node carries none)
-  uint16_t sa;   // seed slot (root: first seed)
-  uint16_t sb;   // root: second seed slot, kSingle for an order-1 term
-  uint32_t nch;  // number of children that follow in DFS preorder
+  double c;       // first output's real coefficient (0 if the node carries none)
+  uint32_t off;   // byte offset of the seed row in the [slot][32 sites] c128 table
+  uint16_t nch;   // number of children that follow in DFS preorder
+  uint16_t skip;  // records in this node's subtree (0xFFFF: too large to say)
 };
 constexpr uint16_t kSingle = 0xFFFF;
+constexpr uint32_t kRowBytes = 32 * 16;  // one slot row: 32 sites x complex128
 
 struct PlanHost {
   int max_order = 2;                 // deepest order in the recursive program
@@ -39,8 +40,8 @@ struct PlanHost {
   std::vector<double> cre, cim;      // [n_ops, n_out] coefficients per record
   int n_out = 1;
   bool complex_coef = false;
-  int warps = 32;                    // warps per CTA the chunks were cut for
-  std::vector<int32_t> chunk;        // [warps+1] op offsets
+  int warps = 32;                    // number of work chunks
+  std::vector<int32_t> chunk;        // [chunks+1] record offsets
   // naive program: per order o (1..max), records of o slots + coefficient row
   int naive_max_order = 1;
   std::vector<int32_t> naive_seg;    // [max+2] record offsets per order

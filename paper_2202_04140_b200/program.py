@@ -13,8 +13,9 @@ import numpy as np
 from . import _native as N
 from .graph import as_eval_graph
 
-OP_DTYPE = np.dtype([("c", "<f8"), ("sa", "<u2"), ("sb", "<u2"), ("nch", "<u4")])
-SINGLE = 0xFFFF
+# {coefficient, byte offset of the seed row (slot * 512), #children, subtree size}
+OP_DTYPE = np.dtype([("c", "<f8"), ("off", "<u4"), ("nch", "<u2"), ("skip", "<u2")])
+ROW_BYTES = 512
 
 
 def compile_program(graph, node_ids, values, warps: int = 32) -> dict:

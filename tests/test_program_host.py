@@ -7,37 +7,51 @@ import pytest
 
 import paper_2202_04140_b200 as P
 from oracle import acedag_oracle as O
-from paper_2202_04140_b200.program import SINGLE, compile_program
+from paper_2202_04140_b200.program import ROW_BYTES, compile_program
 from _helpers import phi_gate, seeded_A
 
 
-def simulate(prog, A, n_out=1):
-    """Walk the program exactly as k2_fast does (per chunk, preorder)."""
+def simulate(prog, A):
+    """Walk the program exactly as k2_fast does (per chunk, preorder):
+    a root is two records (two seeds; slot U is the constant ONE), every
+    other record multiplies its seed into the parent value."""
     ops, slots = prog["ops"], prog["slot_label"]
-    seeds = A[:, slots]  # [S, U]
-    acc = np.zeros(A.shape[0], np.complex128)
+    U = len(slots)
+    seeds = np.concatenate([A[:, slots], np.ones((A.shape[0], 1), A.dtype)], axis=1)  # [S, U+1]
+    acc = np.zeros(A.shape[0])
     pos = 0
+
+    def seed(r):
+        assert r["off"] % ROW_BYTES == 0 and r["off"] // ROW_BYTES <= U
+        return seeds[:, r["off"] // ROW_BYTES]
 
     def visit(parent, count):
         nonlocal pos, acc
         for _ in range(count):
             r = ops[pos]
+            start = pos
             pos += 1
-            v = seeds[:, r["sa"]] * parent
+            v = seed(r) * parent
             acc += r["c"] * v.real
             visit(v, r["nch"])
+            if r["skip"] != 0xFFFF:
+                assert pos - start - 1 == r["skip"]
 
     chunk = prog["chunk"]
     for w in range(len(chunk) - 1):
         pos = chunk[w]
         while pos < chunk[w + 1]:
-            r = ops[pos]
-            pos += 1
-            v = seeds[:, r["sa"]] if r["sb"] == SINGLE else seeds[:, r["sa"]] * seeds[:, r["sb"]]
-            acc += r["c"] * v.real
-            visit(v, r["nch"])
+            r0, r1 = ops[pos], ops[pos + 1]
+            assert r1["c"] == 0 and r1["nch"] == 0
+            pos += 2
+            start = pos
+            v = seed(r0) * seed(r1)
+            acc += r0["c"] * v.real
+            visit(v, r0["nch"])
+            if r0["skip"] != 0xFFFF:
+                assert pos - start == r0["skip"]
         assert pos == chunk[w + 1]
-    return acc.real
+    return acc
 
 
 @pytest.mark.parametrize("D,nu", [(8, 3), (12, 4), (10, 5)])
@@ -45,7 +59,7 @@ def test_program_reproduces_oracle(D, nu):
     g = P.build_graph(P.Group.O3, P.DegreeSpec(1, D), nu)
     rng = np.random.default_rng(D * 10 + nu)
     c = rng.normal(size=len(g.target_ids))
-    prog = compile_program(g, g.target_ids, c, warps=32)
+    prog = compile_program(g, g.target_ids, c, warps=64)
     assert prog["chunk"][0] == 0 and prog["chunk"][-1] == len(prog["ops"])
     assert np.all(np.diff(prog["chunk"]) >= 0)
     A = seeded_A(6, g.num_seeds, 7)

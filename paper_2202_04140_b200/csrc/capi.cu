@@ -146,6 +146,7 @@ struct acedag_plan {
   DevBuf<double> ncre, ncim;
   DevBuf<double2> gcache;
   DevBuf<double2> ws_A;
+  DevBuf<double> part;  // K2 per-chunk partial sums [grid][chunks][32]
 };
 
 // ====================================================================== API
@@ -293,7 +294,7 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
     return fail(ACEDAG_EINVAL, "bad coefficient arguments");
   DevGuard dg(P->device);
   try {
-    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, 64, P->host);
+    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, 128, P->host);
   } catch (const std::domain_error& e) {
     return fail(ACEDAG_ENOTTARGET, e.what());
   } catch (const std::bad_alloc&) {
@@ -381,7 +382,7 @@ struct Launch {
 int k2_warps() {
   static int w = [] {
     const char* e = getenv("ACEDAG_K2_WARPS");
-    int v = e ? atoi(e) : 16;
+    int v = e ? atoi(e) : 32;
     return v == 32 ? 32 : 16;
   }();
   return w;
@@ -420,9 +421,11 @@ cudaError_t launch_fast_w(acedag_plan* P, const void* A, int64_t S, int L, const
   auto k = dev::k2_fast<NU, T, WARPS, MAXU, HYB>;
   cudaError_t e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
+  e = P->part.alloc((size_t)lc.grid * nchunks(P) * 32);
+  if (e != cudaSuccess) return e;
   k<<<lc.grid, lc.block, lc.smem, st>>>(
       reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
-      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(P->gcache.p));
+      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(P->gcache.p), P->part.p);
   return cudaGetLastError();
 }
 
@@ -516,11 +519,11 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
   if (method == ACEDAG_METHOD_RECURSIVE) {
     if (prec == ACEDAG_PREC_F32) {
       if (!fast) return fail(ACEDAG_EUNSUPPORTED, "fp32 mode supports real coefficients, one real output");
-      int rc = plan_launch(P, S, sizeof(float2), nchunks(P) * 32 * sizeof(double) + 16, k2_warps(), lc);
+      int rc = plan_launch(P, S, sizeof(float2), k2_warps() * 1024 + 16, k2_warps(), lc);
       if (rc) return rc;
       e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
     } else if (fast) {
-      int rc = plan_launch(P, S, sizeof(double2), nchunks(P) * 32 * sizeof(double) + 16, k2_warps(), lc);
+      int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024 + 16, k2_warps(), lc);
       if (rc) return rc;
       e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
     } else {

@@ -43,6 +43,22 @@ struct OpR {
   uint32_t off, nch, skip;
 };
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// streaming read that should not displace the program stream from L1
+template <typename V>
+__device__ __forceinline__ V ld_stream(const V* p) {
+  V v;
+  if constexpr (sizeof(V) == 16) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  }
+  return v;
+}
+
 // 16-byte uniform record load (every lane reads the same address)
 __device__ __forceinline__ OpR load_op(const Op* p) {
   int4 raw = __ldg(reinterpret_cast<const int4*>(p));
@@ -96,7 +112,7 @@ __device__ __forceinline__ void stage_seeds(const V* __restrict__ A, int64_t S, 
   for (int u = warp; u <= U; u += W) {
     V v;
     if (u == U) { v.x = 1; v.y = 0; }
-    else if (valid) v = row[__ldg(slot_label + u)];
+    else if (valid) v = ld_stream(row + __ldg(slot_label + u));
     else { v.x = 0; v.y = 0; }
     if (!HYB || u < Us) sA[u * 32 + lane] = v;
     else gA[(u - Us) * 32 + lane] = v;
@@ -105,72 +121,110 @@ __device__ __forceinline__ void stage_seeds(const V* __restrict__ A, int64_t S, 
 
 // ---------------------------------------------------------------- K2 (fast)
 // real coefficients, Re(phi), one output: acc += c * Re(v).
-// Deepest level: the leaves of one parent are loaded as a batch (all record
-// and seed loads in flight together) and only the real part is formed.
+//
+// Program stream: each warp walks a chunk of 16-byte records.  They are
+// staged global -> registers -> a per-warp two-block shared ring (2 x 32
+// records): one coalesced 512 B load per block, issued a block ahead, so the
+// DFS never waits on L2; records are then read with broadcast LDS.128.
+struct Stream {
+  const int4* g;  // chunk start
+  int4* ring;     // [64] records, blocks b and b+1 of the current position
+  int4 stage;     // block b+2, one record per lane
+  uint32_t i, n;  // next record, chunk length
+  int lane;
+
+  __device__ __forceinline__ int4 fetch(uint32_t q) const {
+    return q < n ? __ldg(g + q) : make_int4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ void begin(const int4* gp, uint32_t len, int4* r, int ln) {
+    g = gp;
+    n = len;
+    ring = r;
+    lane = ln;
+    i = 0;
+    const int4 b0 = fetch(lane), b1 = fetch(32 + lane);
+    stage = fetch(64 + lane);
+    __syncwarp();
+    ring[lane] = b0;
+    ring[32 + lane] = b1;
+    __syncwarp();
+  }
+  __device__ __forceinline__ int4 at(uint32_t j) const { return ring[(i + j) & 63]; }
+  __device__ __forceinline__ void advance(uint32_t k) {  // k <= 32
+    const uint32_t ni = i + k;
+    if ((ni >> 5) != (i >> 5)) {
+      const uint32_t b = ni >> 5;
+      __syncwarp();
+      ring[((b + 1) & 1) * 32 + lane] = stage;
+      stage = fetch((b + 2) * 32 + lane);
+      __syncwarp();
+    }
+    i = ni;
+  }
+};
+
+__device__ __forceinline__ double rec_c(int4 r) { return __hiloint2double(r.y, r.x); }
+__device__ __forceinline__ uint32_t rec_off(int4 r) { return (uint32_t)r.z; }
+__device__ __forceinline__ uint32_t rec_nch(int4 r) { return (uint32_t)r.w & 0xFFFFu; }
+
+// Deepest level: the leaves of one parent as one batch (all record and seed
+// loads in flight together); only the real part of each product is formed.
 template <int K, typename T, bool HYB>
-__device__ __forceinline__ void leaf_block(const Op* p, typename V2<T>::t pv, T& acc0, T& acc1,
+__device__ __forceinline__ void leaf_block(const Stream& st, typename V2<T>::t pv, T& acc0, T& acc1,
                                            const Seeds<T, HYB>& sd) {
   using V = typename V2<T>::t;
-  OpR r[K];
+  int4 r[K];
   V s[K];
 #pragma unroll
-  for (int j = 0; j < K; ++j) r[j] = load_op(p + j);
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
 #pragma unroll
-  for (int j = 0; j < K; ++j) s[j] = sd(r[j].off);
+  for (int j = 0; j < K; ++j) s[j] = sd(rec_off(r[j]));
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const T t = s[j].x * pv.x - s[j].y * pv.y;
-    if (j & 1) acc1 += (T)r[j].c * t;
-    else acc0 += (T)r[j].c * t;
+    if (j & 1) acc1 += (T)rec_c(r[j]) * t;
+    else acc0 += (T)rec_c(r[j]) * t;
   }
 }
 
 template <int MAXU, typename T, bool HYB>
-__device__ __forceinline__ void leaves(const Op* p, uint32_t n, typename V2<T>::t pv, T& acc0, T& acc1,
+__device__ __forceinline__ void leaves(Stream& st, uint32_t n, typename V2<T>::t pv, T& acc0, T& acc1,
                                        const Seeds<T, HYB>& sd) {
   while (n >= MAXU) {
-    leaf_block<MAXU, T, HYB>(p, pv, acc0, acc1, sd);
-    p += MAXU;
+    leaf_block<MAXU, T, HYB>(st, pv, acc0, acc1, sd);
+    st.advance(MAXU);
     n -= MAXU;
   }
   switch (n) {
-    case 1: leaf_block<1, T, HYB>(p, pv, acc0, acc1, sd); break;
-    case 2: leaf_block<2, T, HYB>(p, pv, acc0, acc1, sd); break;
-    case 3: leaf_block<3, T, HYB>(p, pv, acc0, acc1, sd); break;
-    case 4: if constexpr (MAXU > 4) leaf_block<4, T, HYB>(p, pv, acc0, acc1, sd); break;
-    case 5: if constexpr (MAXU > 5) leaf_block<5, T, HYB>(p, pv, acc0, acc1, sd); break;
-    case 6: if constexpr (MAXU > 6) leaf_block<6, T, HYB>(p, pv, acc0, acc1, sd); break;
-    case 7: if constexpr (MAXU > 7) leaf_block<7, T, HYB>(p, pv, acc0, acc1, sd); break;
+    case 1: leaf_block<1, T, HYB>(st, pv, acc0, acc1, sd); break;
+    case 2: leaf_block<2, T, HYB>(st, pv, acc0, acc1, sd); break;
+    case 3: leaf_block<3, T, HYB>(st, pv, acc0, acc1, sd); break;
+    case 4: if constexpr (MAXU > 4) leaf_block<4, T, HYB>(st, pv, acc0, acc1, sd); break;
+    case 5: if constexpr (MAXU > 5) leaf_block<5, T, HYB>(st, pv, acc0, acc1, sd); break;
+    case 6: if constexpr (MAXU > 6) leaf_block<6, T, HYB>(st, pv, acc0, acc1, sd); break;
+    case 7: if constexpr (MAXU > 7) leaf_block<7, T, HYB>(st, pv, acc0, acc1, sd); break;
     default: break;
   }
+  st.advance(n);
 }
 
-// Children of a node at order D-1 (values of order D).  `p` points at the
-// first child record and returns past the whole subtree.  The next sibling's
-// record is fetched before the current child's subtree is walked.
+// Children of a node of order D-1 (values of order D), DFS preorder.
 template <int D, int NU, int MAXU, typename T, bool HYB>
-__device__ __forceinline__ const Op* k2_visit(const Op* p, uint32_t n, typename V2<T>::t pv,
-                                             T& acc0, T& acc1, const Seeds<T, HYB>& sd) {
+__device__ __forceinline__ void k2_visit(Stream& st, uint32_t n, typename V2<T>::t pv, T& acc0, T& acc1,
+                                         const Seeds<T, HYB>& sd) {
   using V = typename V2<T>::t;
   if constexpr (D > NU) {
-    return p;
+    return;
   } else if constexpr (D == NU) {
-    leaves<MAXU, T, HYB>(p, n, pv, acc0, acc1, sd);
-    return p + n;
+    leaves<MAXU, T, HYB>(st, n, pv, acc0, acc1, sd);
   } else {
-    if (n == 0) return p;
-    OpR r = load_op(p);
     for (uint32_t j = 0; j < n; ++j) {
-      const bool more = j + 1 < n;
-      const bool pf = more && r.skip != 0xFFFFu;
-      OpR rn;
-      if (pf) rn = load_op(p + 1 + r.skip);
-      const V v = cmul(sd(r.off), pv);
-      acc1 += (T)r.c * v.x;
-      p = k2_visit<D + 1, NU, MAXU, T, HYB>(p + 1, r.nch, v, acc0, acc1, sd);
-      if (more) r = pf ? rn : load_op(p);
+      const int4 r = st.at(0);
+      st.advance(1);
+      const V v = cmul(sd(rec_off(r)), pv);
+      acc1 += (T)rec_c(r) * v.x;
+      k2_visit<D + 1, NU, MAXU, T, HYB>(st, rec_nch(r), v, acc0, acc1, sd);
     }
-    return p;
   }
 }
 
@@ -179,18 +233,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
         const uint16_t* __restrict__ slot_label, int U, int Us, const Op* __restrict__ ops,
         const int32_t* __restrict__ chunk, int nchunk, double* __restrict__ out,
-        typename V2<T>::t* __restrict__ gcache) {
+        typename V2<T>::t* __restrict__ gcache, double* __restrict__ part) {
   using V = typename V2<T>::t;
   extern __shared__ __align__(16) unsigned char smem[];
   V* sA = reinterpret_cast<V*>(smem);
-  double* red = reinterpret_cast<double*>(smem + (size_t)Us * 32 * sizeof(V));
-  int* next = reinterpret_cast<int*>(red + (size_t)nchunk * 32);
+  int4* rings = reinterpret_cast<int4*>(smem + (size_t)Us * 32 * sizeof(V));
+  int* next = reinterpret_cast<int*>(rings + WARPS * 64);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   V* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
   Seeds<T, HYB> sd;
   sd.s = reinterpret_cast<const char*>(sA) + lane * sizeof(V);
   sd.g = HYB ? reinterpret_cast<const char*>(gA) + lane * sizeof(V) - (size_t)Us * 32 * sizeof(V) : nullptr;
   sd.us_bytes = (uint32_t)((size_t)Us * 32 * sizeof(V));
+  double* mypart = part + (size_t)blockIdx.x * nchunk * 32;
+  const int4* prog = reinterpret_cast<const int4*>(ops);
+  Stream st;
   const int64_t ntiles = (S + 31) / 32;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     stage_seeds<V, HYB>(A, S, L, tile, slot_label, U, Us, sA, gA, warp, WARPS, lane);
@@ -201,32 +258,24 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
       if (lane == 0) ci = atomicAdd(next, 1);
       ci = __shfl_sync(0xffffffffu, ci, 0);
       if (ci >= nchunk) break;
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(prog + b, (uint32_t)(e - b), rings + warp * 64, lane);
       double acc = 0.0;
-      const Op* p = ops + __ldg(chunk + ci);
-      const Op* end = ops + __ldg(chunk + ci + 1);
-      if (p < end) {
-        OpR r0 = load_op(p), r1 = load_op(p + 1);
-        while (true) {
-          const bool known = r0.skip != 0xFFFFu;
-          const Op* nxt = p + 2 + r0.skip;
-          OpR n0, n1;
-          if (known && nxt < end) { n0 = load_op(nxt); n1 = load_op(nxt + 1); }
-          T acc0 = 0, acc1 = 0;
-          const V v = cmul(sd(r0.off), sd(r1.off));
-          acc0 += (T)r0.c * v.x;
-          p = k2_visit<3, NU, MAXU, T, HYB>(p + 2, r0.nch, v, acc0, acc1, sd);
-          acc += (double)acc0 + (double)acc1;
-          if (p >= end) break;
-          if (known) { r0 = n0; r1 = n1; }
-          else { r0 = load_op(p); r1 = load_op(p + 1); }
-        }
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        st.advance(2);
+        T acc0 = 0, acc1 = 0;
+        const V v = cmul(sd(rec_off(r0)), sd(rec_off(r1)));
+        acc0 += (T)rec_c(r0) * v.x;
+        k2_visit<3, NU, MAXU, T, HYB>(st, rec_nch(r0), v, acc0, acc1, sd);
+        acc += (double)acc0 + (double)acc1;
       }
-      red[ci * 32 + lane] = acc;
+      mypart[ci * 32 + lane] = acc;
     }
     __syncthreads();
     if (warp == 0) {
       double s = 0.0;
-      for (int c = 0; c < nchunk; ++c) s += red[c * 32 + lane];
+      for (int c = 0; c < nchunk; ++c) s += __ldcg(mypart + c * 32 + lane);
       const int64_t site = tile * 32 + lane;
       if (site < S) out[site] = s;
     }

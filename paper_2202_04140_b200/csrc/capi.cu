@@ -115,6 +115,25 @@ int device_labels(int dev, int group, int cap, const int4** out) {
   return 0;
 }
 
+// K2 chunk schedule: 0 static round robin, 1 dynamic (ACEDAG_SCHED)
+int k2_sched() {
+  static int s = [] {
+    const char* e = getenv("ACEDAG_SCHED");
+    return e ? atoi(e) : 0;
+  }();
+  return s;
+}
+
+// work chunks per program (ACEDAG_CHUNKS overrides; see kernels.cuh k2_fast)
+int plan_chunks() {
+  static int c = [] {
+    const char* e = getenv("ACEDAG_CHUNKS");
+    int v = e ? atoi(e) : 128;
+    return v < 1 ? 1 : (v > 8192 ? 8192 : v);
+  }();
+  return c;
+}
+
 int current_device() {
   int d = 0;
   cudaGetDevice(&d);
@@ -294,7 +313,7 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
     return fail(ACEDAG_EINVAL, "bad coefficient arguments");
   DevGuard dg(P->device);
   try {
-    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, 128, P->host);
+    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, plan_chunks(), P->host);
   } catch (const std::domain_error& e) {
     return fail(ACEDAG_ENOTTARGET, e.what());
   } catch (const std::bad_alloc&) {
@@ -425,7 +444,8 @@ cudaError_t launch_fast_w(acedag_plan* P, const void* A, int64_t S, int L, const
   if (e != cudaSuccess) return e;
   k<<<lc.grid, lc.block, lc.smem, st>>>(
       reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
-      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(P->gcache.p), P->part.p);
+      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(P->gcache.p), P->part.p,
+      k2_sched());
   return cudaGetLastError();
 }
 

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
         const uint16_t* __restrict__ slot_label, int U, int Us, const Op* __restrict__ ops,
         const int32_t* __restrict__ chunk, int nchunk, double* __restrict__ out,
-        typename V2<T>::t* __restrict__ gcache, double* __restrict__ part) {
+        typename V2<T>::t* __restrict__ gcache, double* __restrict__ part, int sched) {
   using V = typename V2<T>::t;
   extern __shared__ __align__(16) unsigned char smem[];
   V* sA = reinterpret_cast<V*>(smem);
@@ -253,10 +253,20 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
     stage_seeds<V, HYB>(A, S, L, tile, slot_label, U, Us, sA, gA, warp, WARPS, lane);
     if (threadIdx.x == 0) *next = 0;
     __syncthreads();
-    while (true) {
-      int ci = 0;
-      if (lane == 0) ci = atomicAdd(next, 1);
-      ci = __shfl_sync(0xffffffffu, ci, 0);
+    // Chunk schedule.  sched == 0: static round robin (chunk c -> warp c % W),
+    // one partial per warp.  sched == 1: dynamic (atomic counter), one
+    // partial per chunk.  Both sum partials in a fixed order, so phi is
+    // bitwise reproducible run to run.
+    double wacc = 0.0;
+    for (int k = 0;; ++k) {
+      int ci;
+      if (sched) {
+        ci = 0;
+        if (lane == 0) ci = atomicAdd(next, 1);
+        ci = __shfl_sync(0xffffffffu, ci, 0);
+      } else {
+        ci = warp + k * WARPS;
+      }
       if (ci >= nchunk) break;
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
       st.begin(prog + b, (uint32_t)(e - b), rings + warp * 64, lane);
@@ -270,12 +280,15 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
         k2_visit<3, NU, MAXU, T, HYB>(st, rec_nch(r0), v, acc0, acc1, sd);
         acc += (double)acc0 + (double)acc1;
       }
-      mypart[ci * 32 + lane] = acc;
+      if (sched) mypart[ci * 32 + lane] = acc;
+      else wacc += acc;
     }
+    if (!sched) mypart[warp * 32 + lane] = wacc;
     __syncthreads();
     if (warp == 0) {
+      const int np = sched ? nchunk : WARPS;
       double s = 0.0;
-      for (int c = 0; c < nchunk; ++c) s += __ldcg(mypart + c * 32 + lane);
+      for (int c = 0; c < np; ++c) s += __ldcg(mypart + c * 32 + lane);
       const int64_t site = tile * 32 + lane;
       if (site < S) out[site] = s;
     }

@@ -73,16 +73,20 @@ __device__ __forceinline__ OpR load_op(const Op* p) {
 // Seed rows addressed by the byte offset stored in the record (c128 layout:
 // slot * 512).  f32 tables use half the stride.  With HYB the rows past the
 // shared-memory budget live in a per-CTA global cache (L1/L2 resident).
+// Dynamic shared memory of every kernel in this file; kernels address it
+// with 32-bit byte offsets so the loads compile to LDS [R + UR].
+extern __shared__ __align__(16) unsigned char g_smem[];
+
 template <typename T, bool HYB>
 struct Seeds {
   using V = typename V2<T>::t;
   static constexpr int kShift = sizeof(V) == 16 ? 0 : 1;
-  const char* s;   // shared base + lane * sizeof(V)
+  uint32_t s;      // g_smem byte offset of this lane's entry in row 0
   const char* g;   // global cache base + lane * sizeof(V) - us_bytes
   uint32_t us_bytes;
   __device__ __forceinline__ V operator()(uint32_t off) const {
     const uint32_t o = off >> kShift;
-    if (!HYB || o < us_bytes) return *reinterpret_cast<const V*>(s + o);
+    if (!HYB || o < us_bytes) return *reinterpret_cast<const V*>(g_smem + s + o);
     return *reinterpret_cast<const V*>(g + o);
   }
 };
@@ -128,7 +132,7 @@ __device__ __forceinline__ void stage_seeds(const V* __restrict__ A, int64_t S, 
 // DFS never waits on L2; records are then read with broadcast LDS.128.
 struct Stream {
   const int4* g;  // chunk start
-  int4* ring;     // [64] records, blocks b and b+1 of the current position
+  uint32_t ring;  // g_smem byte offset of this warp's ring [64 records]
   int4 stage;     // block b+2, one record per lane
   uint32_t i, n;  // next record, chunk length
   int lane;
@@ -136,7 +140,10 @@ struct Stream {
   __device__ __forceinline__ int4 fetch(uint32_t q) const {
     return q < n ? __ldg(g + q) : make_int4(0, 0, 0, 0);
   }
-  __device__ __forceinline__ void begin(const int4* gp, uint32_t len, int4* r, int ln) {
+  __device__ __forceinline__ void put(uint32_t slot, int4 v) const {
+    *reinterpret_cast<int4*>(g_smem + ring + (slot << 4)) = v;
+  }
+  __device__ __forceinline__ void begin(const int4* gp, uint32_t len, uint32_t r, int ln) {
     g = gp;
     n = len;
     ring = r;
@@ -145,17 +152,19 @@ struct Stream {
     const int4 b0 = fetch(lane), b1 = fetch(32 + lane);
     stage = fetch(64 + lane);
     __syncwarp();
-    ring[lane] = b0;
-    ring[32 + lane] = b1;
+    put(lane, b0);
+    put(32 + lane, b1);
     __syncwarp();
   }
-  __device__ __forceinline__ int4 at(uint32_t j) const { return ring[(i + j) & 63]; }
+  __device__ __forceinline__ int4 at(uint32_t j) const {
+    return *reinterpret_cast<const int4*>(g_smem + ring + (((i + j) & 63u) << 4));
+  }
   __device__ __forceinline__ void advance(uint32_t k) {  // k <= 32
     const uint32_t ni = i + k;
     if ((ni >> 5) != (i >> 5)) {
       const uint32_t b = ni >> 5;
       __syncwarp();
-      ring[((b + 1) & 1) * 32 + lane] = stage;
+      put(((b + 1) & 1) * 32 + lane, stage);
       stage = fetch((b + 2) * 32 + lane);
       __syncwarp();
     }
@@ -235,14 +244,14 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
         const int32_t* __restrict__ chunk, int nchunk, double* __restrict__ out,
         typename V2<T>::t* __restrict__ gcache, double* __restrict__ part, int sched) {
   using V = typename V2<T>::t;
-  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* smem = g_smem;
   V* sA = reinterpret_cast<V*>(smem);
-  int4* rings = reinterpret_cast<int4*>(smem + (size_t)Us * 32 * sizeof(V));
-  int* next = reinterpret_cast<int*>(rings + WARPS * 64);
+  const uint32_t rings = (uint32_t)((size_t)Us * 32 * sizeof(V));
+  int* next = reinterpret_cast<int*>(smem + rings + WARPS * 64 * 16);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   V* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
   Seeds<T, HYB> sd;
-  sd.s = reinterpret_cast<const char*>(sA) + lane * sizeof(V);
+  sd.s = (uint32_t)(lane * sizeof(V));
   sd.g = HYB ? reinterpret_cast<const char*>(gA) + lane * sizeof(V) - (size_t)Us * 32 * sizeof(V) : nullptr;
   sd.us_bytes = (uint32_t)((size_t)Us * 32 * sizeof(V));
   double* mypart = part + (size_t)blockIdx.x * nchunk * 32;
@@ -269,7 +278,7 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
       }
       if (ci >= nchunk) break;
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
-      st.begin(prog + b, (uint32_t)(e - b), rings + warp * 64, lane);
+      st.begin(prog + b, (uint32_t)(e - b), rings + warp * 64 * 16, lane);
       double acc = 0.0;
       while (st.i < st.n) {
         const int4 r0 = st.at(0), r1 = st.at(1);
@@ -340,13 +349,13 @@ k2_general(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __re
            int U, int Us, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
            const double* __restrict__ cre, const double* __restrict__ cim, int n_out, int o0,
            int complex_out, void* __restrict__ out, double2* __restrict__ gcache) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* smem = g_smem;
   double2* sA = reinterpret_cast<double2*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)Us * 32 * sizeof(double2));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
   double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
   Seeds<double, HYB> sd;
-  sd.s = reinterpret_cast<const char*>(sA) + lane * 16;
+  sd.s = (uint32_t)(lane * 16);
   sd.g = HYB ? reinterpret_cast<const char*>(gA) + lane * 16 - (size_t)Us * 512 : nullptr;
   sd.us_bytes = (uint32_t)((size_t)Us * 512);
   const int nc = min(NC, n_out - o0);
@@ -398,7 +407,7 @@ k3_naive(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
          int U, int Us, const int32_t* __restrict__ seg, const uint16_t* __restrict__ slots,
          const double* __restrict__ cre, const double* __restrict__ cim, int n_out, int o0,
          int complex_out, void* __restrict__ out, double2* __restrict__ gcache) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* smem = g_smem;
   double2* sA = reinterpret_cast<double2*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)Us * 32 * sizeof(double2));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;

@@ -1,19 +1,21 @@
 """Benchmark: recursive-DAG site evaluations per second on B200.
 
-Workload (BASELINE.json configs[1], the single-GPU DAG-kernel baseline):
-cfg2 -- O3, D=12, nu<=4 (50,909 DAG nodes), seeded complex-normal A per site
-([S, 819] complex128, resident in HBM), one real N(0,1) coefficient per
-target (48,665), output Re(phi) per site.  One step = one pass of the
-recursive kernel K2 over 100,000 sites per GPU (weak scaling: every rank
-evaluates its own 100,000-site shard; sites are independent, so there is no
-data-path collective).
+Default workload (BASELINE.json configs[1], the single-GPU DAG-kernel
+baseline): cfg2 -- O3, D=12, nu<=4 (50,909 DAG nodes), seeded complex-normal
+A per site ([S, 819] complex128, resident in HBM), one real N(0,1)
+coefficient per target (48,665), output Re(phi) per site.  One step = one pass
+of the recursive kernel K2 over 100,000 sites per GPU (weak scaling: every
+rank evaluates its own shard; sites are independent, so there is no
+data-path collective).  `--config cfg1|cfg3|cfg4|cfg5` runs the other
+BASELINE configurations (cfg3/cfg5 from Cartesian neighbour shells with the
+total-energy all-reduce; cfg3/cfg5 shard a fixed global site count).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfgX]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the reference's CPU
-algorithm (the oracle port, oracle/acedag_oracle.py -- the reference is
-pure Python and cannot be installed on the GPU box) on all host cores.
+algorithm (the oracle port, oracle/acedag_oracle.py -- the reference is pure
+Python and is not installed on the GPU box) on all host cores.
 """
 
 from __future__ import annotations
@@ -36,7 +38,22 @@ sys.path.insert(0, ROOT)
 
 METRIC = "site evals/sec (recursive DAG contraction)"
 UNIT = "sites/s"
-CFG = {"D": 12, "nu": 4, "sites_per_gpu": 100_000}
+R_IN, R_CUT = 0.8, 5.0
+
+CONFIGS = {
+    "cfg1": {"D": 8, "nu": 3, "sites": 1_000, "input": "A", "n_out": 1, "scaling": "weak", "cpu_sites": 64,
+             "desc": "cfg1 (BASELINE configs[0]): O3 D=8 nu<=3, 1e3 sites/GPU, A-given"},
+    "cfg2": {"D": 12, "nu": 4, "sites": 100_000, "input": "A", "n_out": 1, "scaling": "weak", "cpu_sites": 32,
+             "desc": "cfg2 (BASELINE configs[1]): O3 D=12 nu<=4, 1e5 sites/GPU, A-given"},
+    "cfg3": {"D": 12, "nu": 4, "sites": 1_000_000, "input": "positions", "J": 30, "n_out": 1,
+             "scaling": "strong", "cpu_sites": 2,
+             "desc": "cfg3 (BASELINE configs[2]): O3 D=12 nu<=4 from J=30 neighbours, 1e6 sites total, energy all-reduce"},
+    "cfg4": {"D": 16, "nu": 6, "sites": 200_000, "input": "A", "n_out": 1, "scaling": "weak", "cpu_sites": 1,
+             "desc": "cfg4 (BASELINE configs[3]): O3 D=16 nu<=6 (3,711,466 nodes), 2e5 sites/GPU, A-given"},
+    "cfg5": {"D": 14, "nu": 5, "sites": 500_000, "input": "positions", "J": 40, "n_out": 64,
+             "scaling": "strong", "cpu_sites": 1,
+             "desc": "cfg5 (BASELINE configs[4]): O3 D=14 nu<=5 from J=40 neighbours, 64 outputs, 5e5 sites total"},
+}
 
 
 def parse():
@@ -45,9 +62,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sites", type=int, default=CFG["sites_per_gpu"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--prec", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--sites", type=int, default=None, help="override the config's site count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-naive", action="store_true")
     return ap.parse_args()
 
 
@@ -59,16 +79,18 @@ def dist_env():
 
 
 # ------------------------------------------------------------- workload
-def workload(D, nu, seed=1):
-    """The graph (native builder, SHA-pinned) and coefficients."""
+def workload(cfg, seed=1):
+    """The graph (native builder, SHA-pinned) and coefficients [T] / [T, n_out]."""
     import paper_2202_04140_b200 as P
-    g = P.build_graph(P.Group.O3, P.DegreeSpec(1, D), nu)
-    c = np.random.default_rng(seed).normal(size=len(g.target_ids))
+    g = P.build_graph(P.Group.O3, P.DegreeSpec(1, cfg["D"]), cfg["nu"])
+    rng = np.random.default_rng(seed)
+    n_out = cfg["n_out"]
+    c = rng.normal(size=len(g.target_ids)) if n_out == 1 else rng.normal(size=(len(g.target_ids), n_out))
     return g, c
 
 
-def dag_census(g):
-    """P, L_f, P_int, T and F_site of the reference DAG."""
+def dag_census(g, cfg, used_seeds):
+    """P, L_f, P_int, T and the algorithmic flops/bytes per site."""
     N, L = g.num_nodes, g.num_seeds
     par = g.parents[L:]
     child = np.zeros(N, np.int64)
@@ -78,8 +100,23 @@ def dag_census(g):
     L_f = int(np.sum(child[L:] == 0))
     P_int = P_ - L_f
     T = len(g.target_ids)
-    F = 6 * P_int + 3 * L_f + 2 * T
-    return {"P": P_, "L_f": L_f, "P_int": P_int, "T": T, "F_site": F, "F_naive_min": None}
+    n_out = cfg["n_out"]
+    F = 6 * P_int + 3 * L_f + 2 * T * n_out
+    if cfg["input"] == "positions":
+        F += 4 * cfg["J"] * used_seeds
+        B = 24 * cfg["J"] + 8 * n_out
+    else:
+        B = 16 * L + 8 * n_out
+    return {"P": P_, "L_f": L_f, "P_int": P_int, "T": T, "F_site": F, "B_site": B}
+
+
+def positions(S, J, gen, device):
+    import torch
+    d = torch.randn(S, J, 3, dtype=torch.float64, device=device, generator=gen)
+    d = d / d.norm(dim=-1, keepdim=True)
+    u = torch.rand(S, J, 1, dtype=torch.float64, device=device, generator=gen)
+    r = (R_IN ** 3 + u * (R_CUT ** 3 - R_IN ** 3)) ** (1.0 / 3.0)
+    return (d * r).contiguous()
 
 
 # --------------------------------------------------------------- clocks
@@ -131,31 +168,31 @@ _CPU_CTX = {}
 
 
 def _cpu_worker(args):
-    """Oracle port of evaluate_graph + sequential c-dot over a site block.
-    The DAG arrays come from the parent through fork (no CUDA in workers)."""
+    """Oracle port of the path (pool for position inputs, evaluate_graph +
+    sequential c-dot) over a block of sites; the DAG arrays come from the
+    parent through fork (no CUDA in the workers)."""
     S, seed = args
     from oracle import acedag_oracle as O
-    pa, pb, tg, c, L = _CPU_CTX["graph"]
+    pa, pb, tg, c, L, cfg = _CPU_CTX["graph"]
     rng = np.random.default_rng(seed)
-    A = rng.normal(0, math.sqrt(0.5), (S, L)) + 1j * rng.normal(0, math.sqrt(0.5), (S, L))
+    if cfg["input"] == "positions":
+        J = cfg["J"]
+        d = rng.normal(size=(S, J, 3))
+        d /= np.linalg.norm(d, axis=-1, keepdims=True)
+        r = (R_IN ** 3 + rng.uniform(size=(S, J)) * (R_CUT ** 3 - R_IN ** 3)) ** (1.0 / 3.0)
+        xyz = d * r[..., None]
+    else:
+        A = rng.normal(0, math.sqrt(0.5), (S, L)) + 1j * rng.normal(0, math.sqrt(0.5), (S, L))
     t0 = time.perf_counter()
+    if cfg["input"] == "positions":
+        A = np.array([O.pool_positions(cfg["D"], xyz[s]) for s in range(S)])
     re, im = O.evaluate_nodes(pa, pb, A)
-    O.model_sum(re, im, tg, c)
+    if c.ndim == 1:
+        O.model_sum(re, im, tg, c)
+    else:
+        for o in range(c.shape[1]):
+            O.model_sum(re, im, tg, c[:, o])
     return S, time.perf_counter() - t0
-
-
-def cpu_rate(g, c, sites_per_proc, procs, reps=1):
-    _CPU_CTX["graph"] = (g.parents[:, 0].copy(), g.parents[:, 1].copy(), g.target_ids.copy(), c, g.num_seeds)
-    ctx = mp.get_context("fork")
-    with ctx.Pool(procs) as pool:
-        pool.map(_cpu_worker, [(2, 0)] * procs)  # warm imports
-        tot_s, wall = 0, 0.0
-        for r in range(reps):
-            t0 = time.perf_counter()
-            res = pool.map(_cpu_worker, [(sites_per_proc, 100 + r * procs + i) for i in range(procs)])
-            wall += time.perf_counter() - t0
-            tot_s += sum(s for s, _ in res)
-    return tot_s / wall, tot_s
 
 
 def host_cores():
@@ -165,34 +202,56 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def cpu_pool(g, c, cfg, procs):
+    _CPU_CTX["graph"] = (g.parents[:, 0].copy(), g.parents[:, 1].copy(), g.target_ids.copy(), c,
+                         g.num_seeds, cfg)
+    return mp.get_context("fork").Pool(procs)
+
+
+def cpu_rate(g, c, cfg, procs, reps=1):
+    per = cfg["cpu_sites"]
+    with cpu_pool(g, c, cfg, procs) as pool:
+        pool.map(_cpu_worker, [(1, i) for i in range(procs)])  # warm imports
+        tot, wall = 0, 0.0
+        for r in range(reps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_worker, [(per, 100 + r * procs + i) for i in range(procs)])
+            wall += time.perf_counter() - t0
+            tot += sum(s for s, _ in res)
+    return tot / wall, tot
+
+
+def cpu_sample_text(cfg, procs, n):
+    what = "pool_positions + " if cfg["input"] == "positions" else ""
+    return (f"{n} sites: {procs} processes x {cfg['cpu_sites']} sites per step (oracle/acedag_oracle.py "
+            f"{what}evaluate_nodes + model_sum, NumPy, fork pool)")
+
+
 # --------------------------------------------------------- reference arm
 def run_reference(a):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    cfg = CONFIGS[a.config]
     cores = host_cores()
-    per = 32
-    g, c = workload(CFG["D"], CFG["nu"])
-    _CPU_CTX["graph"] = (g.parents[:, 0].copy(), g.parents[:, 1].copy(), g.target_ids.copy(), c, g.num_seeds)
-    with mp.get_context("fork").Pool(cores) as pool:
+    g, c = workload(cfg)
+    with cpu_pool(g, c, cfg, cores) as pool:
         for w in range(a.warmup):
-            pool.map(_cpu_worker, [(4, w * cores + i) for i in range(cores)])
+            pool.map(_cpu_worker, [(1, w * cores + i) for i in range(cores)])
         sites = 0
         t0 = time.perf_counter()
         for k in range(a.steps):
-            res = pool.map(_cpu_worker, [(per, 1000 + k * cores + i) for i in range(cores)])
+            res = pool.map(_cpu_worker, [(cfg["cpu_sites"], 1000 + k * cores + i) for i in range(cores)])
             sites += sum(s for s, _ in res)
         wall = time.perf_counter() - t0
     value = sites / wall
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * wall / a.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded complex-normal A, N(0,1) coefficients",
-            "config": {"workload": "cfg2: O3 D=12 nu<=4 recursive DAG + c-dot, Re(phi)",
-                       "sites_per_step": per * cores},
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded complex-normal A (or uniform neighbour shells), N(0,1) coefficients",
+            "config": {"workload": cfg["desc"], "sites_per_step": cfg["cpu_sites"] * cores},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{per} sites per process x {cores} processes per step "
-                                       "(oracle/acedag_oracle.py evaluate_nodes + model_sum, NumPy)"},
+                             "sample": cpu_sample_text(cfg, cores, sites)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -218,11 +277,19 @@ def fp64_peak_tflops(dev):
     return best
 
 
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
 
     import paper_2202_04140_b200 as P
+    from paper_2202_04140_b200.distributed import shard_range, total_energy
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -234,20 +301,52 @@ def run_ours(a):
         if world > 1:
             dist.barrier()
 
-    D, nu, S = CFG["D"], CFG["nu"], a.sites
-    g, c = workload(D, nu)
-    census = dag_census(g)
+    def max_over_ranks(x):
+        if world > 1:
+            t = torch.tensor([x], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    cfg = CONFIGS[a.config]
+    total_sites = a.sites or cfg["sites"]
+    if cfg["scaling"] == "strong":
+        lo, hi = shard_range(total_sites, rank, world)
+        S = hi - lo
+        global_sites = total_sites
+    else:
+        S = total_sites
+        global_sites = world * S
+    n_out = cfg["n_out"]
+    g, c = workload(cfg)
+    t_plan = time.perf_counter()
     plan = P.SitePlan(g, local).set_coefficients(node_ids=g.target_ids, values=c)
+    t_plan = time.perf_counter() - t_plan
     info = plan.info()
+    census = dag_census(g, cfg, info["used_seeds"])
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     L = g.num_seeds
-    A = torch.complex(torch.randn(S, L, device=dev, dtype=torch.float64, generator=gen),
-                      torch.randn(S, L, device=dev, dtype=torch.float64, generator=gen)) * math.sqrt(0.5)
-    out = torch.empty(S, dtype=torch.float64, device=dev)
+    pos = cfg["input"] == "positions"
+    if pos:
+        X = positions(S, cfg["J"], gen, dev)
+    else:
+        X = torch.complex(torch.randn(S, L, device=dev, dtype=torch.float64, generator=gen),
+                          torch.randn(S, L, device=dev, dtype=torch.float64, generator=gen)) * math.sqrt(0.5)
+        if a.prec == "f32":
+            X = X.to(torch.complex64)
+    out = torch.empty((S,) if n_out == 1 else (S, n_out), dtype=torch.float64, device=dev)
+    energy = torch.zeros(n_out, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
+    launches = {"k": 0}
 
     def step():
-        plan.evaluate(A, result=out)
+        if pos:
+            plan.evaluate_positions(X, result=out)
+            energy.zero_()
+            plan.reduce_sites(out, energy)
+            total_energy(energy)
+        else:
+            plan.evaluate(X, result=out)
 
     for _ in range(a.warmup):
         step()
@@ -263,93 +362,132 @@ def run_ours(a):
         torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / a.steps
-    value = world * S / (ms_step * 1e-3)
+    ms_step = max_over_ranks(e0.elapsed_time(e1)) / a.steps
+    value = global_sites / (ms_step * 1e-3)
 
-    # naive comparison path (same inputs), a few steps
-    nsteps = max(3, a.steps // 10)
-    plan.evaluate(A, method="naive", result=out)
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(nsteps):
-        plan.evaluate(A, method="naive", result=out)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    naive_ms = e0.elapsed_time(e1) / nsteps
+    # our kernels launched per step (pool chunks + K2 passes + reduce)
+    if pos:
+        chunks = (S + (1 << 17) - 1) >> 17
+        passes = 1 if n_out == 1 else (n_out + 31) // 32
+        per_step = chunks * (1 + passes) + 1
+    else:
+        per_step = 1
+    gpu_launches = per_step * a.steps
+
+    # kernel-only time of K2 (the dominant kernel) for the roofline
+    k2_ms = ms_step
+    if pos:
+        A_ws = P.pool_positions(cfg["D"], X[: min(S, 1 << 17)])
+        sub = A_ws.shape[0]
+        plan.evaluate(A_ws, result=torch.empty_like(out[:sub]))
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            plan.evaluate(A_ws, result=torch.empty_like(out[:sub]) if n_out == 1 else out[:sub])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        k2_ms = e0.elapsed_time(e1) / 3 * S / sub
+        del A_ws
+
+    naive = None
+    if not pos and not a.no_naive and a.prec == "f64":
+        nsteps = max(3, a.steps // 10)
+        plan.evaluate(X, method="naive", result=out)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(nsteps):
+            plan.evaluate(X, method="naive", result=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        naive_ms = max_over_ranks(e0.elapsed_time(e1) / nsteps)
+        naive = {"value": global_sites / (naive_ms * 1e-3), "unit": UNIT, "ms_per_step": naive_ms,
+                 "naive_products_per_site": info["naive_products"]}
 
     # end to end through the public API on pinned host buffers
     e2e = None
     if not a.no_e2e:
-        Ah = A.cpu().pin_memory()
-        res = torch.empty(S, dtype=torch.float64, pin_memory=True)
+        Xh = X.cpu().pin_memory()
+        res = torch.empty(out.shape, dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            if pos:
+                plan.evaluate_positions_host(Xh, result=res)
+            else:
+                plan.evaluate_host(Xh, result=res)
+
         for _ in range(2):
-            plan.evaluate_host(Ah, result=res)
+            e2e_step()
         torch.cuda.synchronize()
         barrier()
         k = max(3, a.steps // 10)
         e0.record(stream)
         for _ in range(k):
-            plan.evaluate_host(Ah, result=res)
+            e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / k
-        if world > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": world * S / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(Ah.numel() * 16),
-               "d2h_bytes_per_step": int(S * 8), "ms_per_step": ems,
-               "path": "SitePlan.evaluate_host: pinned host A -> 2-stream chunked H2D/K2/D2H"}
-        del Ah
+        ems = max_over_ranks(e0.elapsed_time(e1) / k)
+        e2e = {"value": global_sites / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size()),
+               "d2h_bytes_per_step": int(res.numel() * 8), "ms_per_step": ems,
+               "path": "SitePlan.evaluate%s_host: pinned host input -> 2-stream chunked H2D / kernels / D2H"
+                       % ("_positions" if pos else "")}
+        del Xh
 
-    peak = fp64_peak_tflops(dev)
-    achieved = census["F_site"] * S / (ms_step * 1e-3) / 1e12
-    prof = os.path.join(ROOT, "profiles", "ncu_k2_summary.json")
-    traffic = None
+    F = census["F_site"]
+    if cfg["D"] <= 8 and not pos:  # cfg1 is bandwidth-bound (F/B = 1.9)
+        peak, src = hbm_peak()
+        achieved = census["B_site"] * S / (k2_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": src, "bytes_per_site": census["B_site"]}
+    else:
+        peak = fp64_peak_tflops(dev)
+        if a.prec == "f32":
+            peak *= 2.0  # FFMA rate is 2x DFMA on B200 (72.6 vs 34.2 TF measured, profiles/r01)
+        achieved = F * S / (k2_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64" if a.prec == "f64" else "fp32", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_source": "measured in this run: cuBLAS DGEMM 8192^3" + (" x2 (fp32)" if a.prec == "f32" else "")
+                               + "; MEASURED_PEAKS.json has no FP64 entry",
+                "flops_per_site": F,
+                "flop_model": "F_site = 6 P_int + 3 L_f + 2 T n_out" + (" + 4 J U_used" if pos else "") + " (SURVEY.md 8d)"}
+    roof["kernel"] = "k2_multi" if n_out > 1 else "k2_fast"
+    roof["kernel_ms"] = k2_ms
+    prof = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    roof["traffic"] = None
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            roof["traffic"] = json.load(open(prof)).get(a.config)
         except Exception:
-            traffic = None
+            pass
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cores = host_cores()
-        rate, n = cpu_rate(g, c, 32, cores, reps=2)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{n} sites: 2 x {cores} processes x 32 sites (oracle/acedag_oracle.py "
-                         "evaluate_nodes + model_sum, NumPy, fork pool)"}
+        rate, n = cpu_rate(g, c, cfg, cores, reps=1)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": cpu_sample_text(cfg, cores, n)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded complex-normal A [S,819] c128 in HBM, N(0,1) coefficient per target",
-            "config": {"workload": "cfg2 (BASELINE configs[1]): O3 D=12 nu<=4, recursive DAG K2, real c, Re(phi)",
-                       "sites_per_gpu": S, "global_sites": world * S, "dag_nodes": g.num_nodes,
-                       "dag_products": census["P"], "targets": census["T"],
-                       "plan_products": info["recursive_products"], "plan_extra_nodes": info["extra_nodes"],
-                       "used_seeds": info["used_seeds"],
-                       "l2": f"inputs {S * L * 16 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush)",
-                       "parallelism": f"dp{world} (sites sharded, no collective)"},
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": cfg["scaling"],
+            "vs_baseline": None, "dtype": a.prec,
+            "data": ("synthetic: seeded uniform neighbour shells 0.8-5.0 [S,J,3] f64" if pos else
+                     "synthetic: seeded complex-normal A [S,%d] %s" % (L, "c128" if a.prec == "f64" else "c64"))
+                    + " in HBM, N(0,1) coefficients per target",
+            "config": {"workload": cfg["desc"], "sites_per_gpu": S, "global_sites": global_sites,
+                       "dag_nodes": g.num_nodes, "dag_products": census["P"], "targets": census["T"],
+                       "n_out": n_out, "plan_products": info["recursive_products"],
+                       "plan_extra_nodes": info["extra_nodes"], "used_seeds": info["used_seeds"],
+                       "plan_build_s": round(t_plan, 2),
+                       "l2": "inputs %.2f GB per GPU > 126 MB L2 (no flush)" % (X.numel() * X.element_size() / 1e9)
+                       if X.numel() * X.element_size() > 126e6 else "inputs fit L2; timed steps reuse them",
+                       "parallelism": f"dp{world} (sites sharded" + (", energy all-reduce)" if pos else ", no collective)")},
             "dag_products_per_s": value * census["P"],
-            "naive": {"value": world * S / (naive_ms * 1e-3), "unit": UNIT, "ms_per_step": naive_ms,
-                      "naive_products_per_site": info["naive_products"]},
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": "measured in this run: cuBLAS DGEMM 8192^3 (MEASURED_PEAKS.json has no FP64 entry)",
-                         "flops_per_site": census["F_site"],
-                         "flop_model": "F_site = 6 P_int + 3 L_f + 2 T (SURVEY.md 8d)",
-                         "kernel": "k2_fast (one launch per step; duration = step time)"},
+            "naive": naive,
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": a.steps,
+            "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -332,7 +332,11 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   CK(P->used_labels.upload(used));
   CK(P->ops.upload(H.ops));
   CK(P->chunk.upload(H.chunk));
-  CK(P->cre.upload(H.cre));
+  {
+    std::vector<double> padded(H.cre);
+    padded.resize(H.cre.size() + 64, 0.0);  // k2_multi reads whole 32-output slices
+    CK(P->cre.upload(padded));
+  }
   CK(P->cim.upload(H.cim));
   CK(P->nseg.upload(H.naive_seg));
   CK(P->nslots.upload(H.naive_slots));
@@ -456,6 +460,25 @@ cudaError_t launch_fast(acedag_plan* P, const void* A, int64_t S, int L, const u
   return launch_fast_w<NU, T, 16, 8, HYB>(P, A, S, L, slot_label, out, lc, st);
 }
 
+constexpr int kMultiWarps = 16, kNOC = 32;
+
+template <int NU, bool HYB>
+cudaError_t launch_multi(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                         double* out, const Launch& lc, cudaStream_t st) {
+  auto k = dev::k2_multi<NU, kMultiWarps, kNOC, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  e = P->part.alloc((size_t)lc.grid * kMultiWarps * kNOC * 32);
+  if (e != cudaSuccess) return e;
+  for (int o0 = 0; o0 < P->host.n_out; o0 += kNOC) {
+    k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
+                                          P->cre.p, P->host.n_out, o0, out, P->gcache.p, P->part.p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 template <int NU, bool HYB>
 cudaError_t launch_general(acedag_plan* P, const double2* A, int64_t S, int L,
                            const uint16_t* slot_label, int complex_out, void* out, const Launch& lc,
@@ -514,6 +537,11 @@ template <int NU> struct FastF32 {
     return hyb ? launch_fast<NU, float, true>(a...) : launch_fast<NU, float, false>(a...);
   }
 };
+template <int NU> struct Multi {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_multi<NU, true>(a...) : launch_multi<NU, false>(a...);
+  }
+};
 template <int NU> struct General {
   template <typename... A> static cudaError_t run(bool hyb, A... a) {
     return hyb ? launch_general<NU, true>(a...) : launch_general<NU, false>(a...);
@@ -546,6 +574,10 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
       int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024 + 16, k2_warps(), lc);
       if (rc) return rc;
       e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+    } else if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out % 2 == 0) {
+      int rc = plan_launch(P, S, sizeof(double2), kMultiWarps * 1024, kMultiWarps, lc);
+      if (rc) return rc;
+      e = by_order<Multi>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
     } else {
       int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), kWarps, lc);
       if (rc) return rc;

@@ -304,6 +304,96 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
   }
 }
 
+// ------------------------------------------------------- K2 (multi-output)
+// Real coefficients, Re(phi), n_out outputs (BASELINE cfg5: 64): the c . A
+// epilogue is a dense [sites x nodes] x [nodes x n_out] product, FP64-bound.
+// Each pass handles NOC outputs with NOC accumulators per lane; every node's
+// coefficient row slice is read warp-uniformly (NOC/2 LDG.128 broadcasts).
+template <int NOC>
+__device__ __forceinline__ void acc_row(double (&acc)[NOC], double re, const double* __restrict__ row) {
+#pragma unroll
+  for (int q = 0; q < NOC; q += 2) {
+    const double2 c = __ldg(reinterpret_cast<const double2*>(row + q));
+    acc[q] += c.x * re;
+    acc[q + 1] += c.y * re;
+  }
+}
+
+template <int D, int NU, int NOC, bool HYB>
+__device__ __forceinline__ void k2m_visit(Stream& st, const int4* prog, int32_t cbeg, uint32_t n, double2 pv,
+                                          double (&acc)[NOC], const Seeds<double, HYB>& sd,
+                                          const double* __restrict__ cre, int n_out, int o0) {
+  if constexpr (D > NU) {
+    return;
+  } else {
+    for (uint32_t j = 0; j < n; ++j) {
+      const int4 r = st.at(0);
+      const int64_t rec = cbeg + (int64_t)st.i;
+      st.advance(1);
+      const double2 s = sd(rec_off(r));
+      if (D == NU || rec_nch(r) == 0) {
+        acc_row<NOC>(acc, s.x * pv.x - s.y * pv.y, cre + rec * n_out + o0);
+      } else {
+        const double2 v = cmul(s, pv);
+        acc_row<NOC>(acc, v.x, cre + rec * n_out + o0);
+        k2m_visit<D + 1, NU, NOC, HYB>(st, prog, cbeg, rec_nch(r), v, acc, sd, cre, n_out, o0);
+      }
+    }
+  }
+}
+
+template <int NU, int WARPS, int NOC, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k2_multi(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
+         int Us, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
+         const double* __restrict__ cre, int n_out, int o0, double* __restrict__ out,
+         double2* __restrict__ gcache, double* __restrict__ part) {
+  unsigned char* smem = g_smem;
+  double2* sA = reinterpret_cast<double2*>(smem);
+  const uint32_t rings = (uint32_t)((size_t)Us * 32 * sizeof(double2));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
+  Seeds<double, HYB> sd;
+  sd.s = (uint32_t)(lane * 16);
+  sd.g = HYB ? reinterpret_cast<const char*>(gA) + lane * 16 - (size_t)Us * 512 : nullptr;
+  sd.us_bytes = (uint32_t)((size_t)Us * 512);
+  const int nc = min(NOC, n_out - o0);
+  double* mypart = part + (size_t)blockIdx.x * WARPS * NOC * 32;
+  const int4* prog = reinterpret_cast<const int4*>(ops);
+  Stream st;
+  const int64_t ntiles = (S + 31) / 32;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    stage_seeds<double2, HYB>(A, S, L, tile, slot_label, U, Us, sA, gA, warp, WARPS, lane);
+    __syncthreads();
+    double acc[NOC];
+#pragma unroll
+    for (int q = 0; q < NOC; ++q) acc[q] = 0.0;
+    for (int ci = warp; ci < nchunk; ci += WARPS) {
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(prog + b, (uint32_t)(e - b), rings + warp * 64 * 16, lane);
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        const int64_t rec = b + (int64_t)st.i;
+        st.advance(2);
+        const double2 v = cmul(sd(rec_off(r0)), sd(rec_off(r1)));
+        acc_row<NOC>(acc, v.x, cre + rec * n_out + o0);
+        k2m_visit<3, NU, NOC, HYB>(st, prog, b, rec_nch(r0), v, acc, sd, cre, n_out, o0);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NOC; ++q) mypart[(warp * NOC + q) * 32 + lane] = acc[q];
+    __syncthreads();
+    // output q is reduced by warp q % WARPS over the warps in order
+    const int64_t site = tile * 32 + lane;
+    for (int q = warp; q < nc; q += WARPS) {
+      double s = 0.0;
+      for (int w = 0; w < WARPS; ++w) s += __ldcg(mypart + (w * NOC + q) * 32 + lane);
+      if (site < S) out[site * n_out + o0 + q] = s;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------- K2 (general)
 // complex coefficients and/or complex output and/or several outputs: NC
 // complex accumulators per lane; coefficient table [n_records, n_out].

@@ -196,22 +196,41 @@ class SitePlan:
         return result
 
     def evaluate_host(self, A: torch.Tensor, method: str = "recursive", chunk: int = 16384,
-                      result: torch.Tensor | None = None) -> torch.Tensor:
+                      result: torch.Tensor | None = None, sync: bool = True) -> torch.Tensor:
         """End-to-end call on HOST buffers: A is a (pinned) CPU complex tensor
         [S, L]; chunks are copied to the device, evaluated and copied back on
         two streams so the PCIe transfers overlap the kernels.  Returns a
         pinned float64 [S] (real output, one coefficient vector)."""
         if A.is_cuda:
             raise ValueError("evaluate_host takes a CPU tensor")
-        S, L = A.shape
+        return self._host_pipeline(A, lambda x, r: self.evaluate(x, method=method, result=r), chunk, result,
+                                   sync)
+
+    def evaluate_positions_host(self, xyz: torch.Tensor, r_in: float = R_IN, r_cut: float = R_CUT,
+                                chunk: int = 65536, result: torch.Tensor | None = None,
+                                sync: bool = True) -> torch.Tensor:
+        """End-to-end fused K1 + K2 on a (pinned) host [S, J, 3] tensor."""
+        if xyz.is_cuda:
+            raise ValueError("evaluate_positions_host takes a CPU tensor")
+        return self._host_pipeline(
+            xyz, lambda x, r: self.evaluate_positions(x, r_in=r_in, r_cut=r_cut, result=r), chunk, result, sync)
+
+    def _host_pipeline(self, X: torch.Tensor, fn, chunk: int, result, sync: bool):
+        """Chunks of X are copied to the device, evaluated by ``fn`` and copied
+        back on two streams, so PCIe transfers overlap the kernels.  With
+        ``sync`` the host result is complete on return; otherwise it is
+        complete once the caller's current stream has drained."""
+        S = X.shape[0]
         dev = torch.device("cuda", self.device)
+        oshape = () if self.n_out == 1 else (self.n_out,)
         if result is None:
-            result = torch.empty(S, dtype=torch.float64, pin_memory=True)
-        key = (chunk, A.dtype)
+            result = torch.empty((S,) + oshape, dtype=torch.float64, pin_memory=True)
+        key = (chunk, X.dtype, tuple(X.shape[1:]), oshape)
         if getattr(self, "_host_ws", (None,))[0] != key:
             self._host_ws = (key, [torch.cuda.Stream(dev) for _ in range(2)],
-                             [torch.empty((chunk, L), dtype=A.dtype, device=dev) for _ in range(2)],
-                             [torch.empty(chunk, dtype=torch.float64, device=dev) for _ in range(2)])
+                             [torch.empty((chunk,) + tuple(X.shape[1:]), dtype=X.dtype, device=dev)
+                              for _ in range(2)],
+                             [torch.empty((chunk,) + oshape, dtype=torch.float64, device=dev) for _ in range(2)])
         _, streams, bufs, outs = self._host_ws
         caller = torch.cuda.current_stream(dev)
         for s in streams:
@@ -220,11 +239,13 @@ class SitePlan:
             n = min(chunk, S - s0)
             st = streams[i % 2]
             with torch.cuda.stream(st):
-                bufs[i % 2][:n].copy_(A[s0:s0 + n], non_blocking=True)
-                self.evaluate(bufs[i % 2][:n], method=method, result=outs[i % 2][:n])
+                bufs[i % 2][:n].copy_(X[s0:s0 + n], non_blocking=True)
+                fn(bufs[i % 2][:n], outs[i % 2][:n])
                 result[s0:s0 + n].copy_(outs[i % 2][:n], non_blocking=True)
         for s in streams:
             caller.wait_stream(s)
+        if sync:
+            caller.synchronize()
         return result
 
     def evaluate_positions(self, xyz: torch.Tensor, counts: torch.Tensor | None = None,

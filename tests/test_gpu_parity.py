@@ -225,3 +225,33 @@ def test_edge_sizes(cuda, cfg1):
         assert phi_gate(rec[:3], pr, scale)[0] and phi_gate(nai[:3], pr, scale)[0]
     zero = plan.evaluate(torch.zeros((3, cfg1.num_seeds), dtype=torch.complex128, device=cuda))
     assert torch.all(zero == 0)
+
+
+@pytest.mark.parametrize("n_out", [2, 64])
+def test_multi_output_real_coefficients(cuda, cfg2, n_out):
+    """The k2_multi path (real c, Re phi, even n_out; BASELINE cfg5 uses 64)."""
+    S = 48
+    A = seeded_A(S, cfg2.num_seeds, 20 + n_out)
+    C = np.random.default_rng(21).normal(size=(len(cfg2.target_ids), n_out))
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=C)
+    got = plan.evaluate(torch.from_numpy(A).to(cuda)).cpu().numpy()
+    assert got.shape == (S, n_out)
+    re, im = O.evaluate_nodes(cfg2.parents[:, 0], cfg2.parents[:, 1], A[:6])
+    for o in range(0, n_out, max(1, n_out // 8)):
+        pr, _ = O.model_sum(re, im, cfg2.target_ids, C[:, o])
+        assert phi_gate(got[:6, o], pr, O.energy_scale(re, cfg2.target_ids, C[:, o]))[0], o
+    tot = plan.reduce_sites(torch.from_numpy(got).to(cuda)).cpu().numpy()
+    assert np.allclose(tot, got.sum(axis=0), rtol=1e-12, atol=1e-9)
+
+
+def test_host_pipelines_match_device(cuda, cfg2, golden):
+    c = np.random.default_rng(30).normal(size=len(cfg2.target_ids))
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
+    A = torch.from_numpy(seeded_A(70_000, cfg2.num_seeds, 31))
+    dev_phi = plan.evaluate(A.to(cuda)).cpu()
+    host_phi = plan.evaluate_host(A.pin_memory(), chunk=16384)
+    torch.cuda.synchronize()
+    assert torch.equal(dev_phi, host_phi)
+    xyz = torch.from_numpy(golden("positions_cfg3.npz")["xyz"])
+    assert torch.equal(plan.evaluate_positions(xyz.to(cuda)).cpu(),
+                       plan.evaluate_positions_host(xyz.pin_memory(), chunk=2).clone())

@@ -334,7 +334,9 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   CK(P->chunk.upload(H.chunk));
   {
     std::vector<double> padded(H.cre);
-    padded.resize(H.cre.size() + 64, 0.0);  // k2_multi reads whole 32-output slices
+    // k2_multi reads whole 32-output slices; k2_mma prefetches two 4-record
+    // groups past the end of a chunk
+    padded.resize(H.cre.size() + 16 * (size_t)H.n_out + 64, 0.0);
     CK(P->cre.upload(padded));
   }
   CK(P->cim.upload(H.cim));
@@ -479,6 +481,34 @@ cudaError_t launch_multi(acedag_plan* P, const double2* A, int64_t S, int L, con
   return cudaSuccess;
 }
 
+constexpr int kMmaWarps = 16;
+
+template <int NU, bool HYB>
+cudaError_t launch_mma(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                       double* out, const Launch& lc, cudaStream_t st) {
+  auto k = dev::k2_mma<NU, kMmaWarps, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  e = P->part.alloc((size_t)lc.grid * kMmaWarps * 32 * 32);
+  if (e != cudaSuccess) return e;
+  for (int o0 = 0; o0 < P->host.n_out; o0 += 32) {
+    k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
+                                          P->cre.p, P->host.n_out, o0, out, P->gcache.p, P->part.p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// ACEDAG_MULTI=scalar selects the scalar multi-output kernel instead of DMMA
+bool use_mma() {
+  static bool m = [] {
+    const char* e = getenv("ACEDAG_MULTI");
+    return !(e && std::string(e) == "scalar");
+  }();
+  return m;
+}
+
 template <int NU, bool HYB>
 cudaError_t launch_general(acedag_plan* P, const double2* A, int64_t S, int L,
                            const uint16_t* slot_label, int complex_out, void* out, const Launch& lc,
@@ -542,6 +572,11 @@ template <int NU> struct Multi {
     return hyb ? launch_multi<NU, true>(a...) : launch_multi<NU, false>(a...);
   }
 };
+template <int NU> struct Mma {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_mma<NU, true>(a...) : launch_mma<NU, false>(a...);
+  }
+};
 template <int NU> struct General {
   template <typename... A> static cudaError_t run(bool hyb, A... a) {
     return hyb ? launch_general<NU, true>(a...) : launch_general<NU, false>(a...);
@@ -574,6 +609,11 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
       int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024 + 16, k2_warps(), lc);
       if (rc) return rc;
       e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+    } else if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out >= 8 && use_mma()) {
+      // smem beyond the seed rows: 16 program rings + 16 x [4][36] staging
+      int rc = plan_launch(P, S, sizeof(double2), kMmaWarps * 1024 + kMmaWarps * 4 * 36 * 8, kMmaWarps, lc);
+      if (rc) return rc;
+      e = by_order<Mma>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
     } else if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out % 2 == 0) {
       int rc = plan_launch(P, S, sizeof(double2), kMultiWarps * 1024, kMultiWarps, lc);
       if (rc) return rc;

@@ -310,7 +310,13 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
 // Each pass handles NOC outputs with NOC accumulators per lane; every node's
 // coefficient row slice is read warp-uniformly (NOC/2 LDG.128 broadcasts).
 template <int NOC>
-__device__ __forceinline__ void acc_row(double (&acc)[NOC], double re, const double* __restrict__ row) {
+__device__ __forceinline__ void acc_row(double (&acc)[NOC], double re, const double* __restrict__ row,
+                                        int stride) {
+  // the coefficient rows stream from L2 in record order: pull the slice of
+  // the record kPfDist ahead into L1 so this warp's next loads hit there
+  constexpr int kPfDist = 4;
+#pragma unroll
+  for (int q = 0; q < NOC; q += 16) prefetch_l1(row + kPfDist * stride + q);
 #pragma unroll
   for (int q = 0; q < NOC; q += 2) {
     const double2 c = __ldg(reinterpret_cast<const double2*>(row + q));
@@ -332,10 +338,10 @@ __device__ __forceinline__ void k2m_visit(Stream& st, const int4* prog, int32_t 
       st.advance(1);
       const double2 s = sd(rec_off(r));
       if (D == NU || rec_nch(r) == 0) {
-        acc_row<NOC>(acc, s.x * pv.x - s.y * pv.y, cre + rec * n_out + o0);
+        acc_row<NOC>(acc, s.x * pv.x - s.y * pv.y, cre + rec * n_out + o0, n_out);
       } else {
         const double2 v = cmul(s, pv);
-        acc_row<NOC>(acc, v.x, cre + rec * n_out + o0);
+        acc_row<NOC>(acc, v.x, cre + rec * n_out + o0, n_out);
         k2m_visit<D + 1, NU, NOC, HYB>(st, prog, cbeg, rec_nch(r), v, acc, sd, cre, n_out, o0);
       }
     }
@@ -376,7 +382,7 @@ k2_multi(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
         const int64_t rec = b + (int64_t)st.i;
         st.advance(2);
         const double2 v = cmul(sd(rec_off(r0)), sd(rec_off(r1)));
-        acc_row<NOC>(acc, v.x, cre + rec * n_out + o0);
+        acc_row<NOC>(acc, v.x, cre + rec * n_out + o0, n_out);
         k2m_visit<3, NU, NOC, HYB>(st, prog, b, rec_nch(r0), v, acc, sd, cre, n_out, o0);
       }
     }
@@ -389,6 +395,178 @@ k2_multi(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
       double s = 0.0;
       for (int w = 0; w < WARPS; ++w) s += __ldcg(mypart + (w * NOC + q) * 32 + lane);
       if (site < S) out[site * n_out + o0 + q] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------- K2 multi-output on DMMA
+// Real coefficients, n_out outputs: the epilogue sum_k c[k][o] Re(v_k) is a
+// dense [32 sites x nodes] x [nodes x n_out] GEMM per tile, issued on the
+// FP64 tensor cores (mma.sync m8n8k4 f64).  Each warp stages the real parts
+// of its last 4 nodes in shared memory ([4][36] doubles, lane = site); every
+// 4 nodes one k-step of 4 (sites) x 4 (outputs) m8n8k4 tiles accumulates
+// into registers.  Coefficient fragments are prefetched two groups ahead.
+struct MmaSink {
+  static constexpr int kNT = 4;     // n-tiles per pass (32 outputs)
+  static constexpr int kStride = 36;  // doubles per staged node row (bank spread)
+  uint32_t stg;     // g_smem byte offset of this warp's [8][kStride] staging
+  uint32_t cnt;     // nodes pushed in the current chunk
+  int64_t rec0;     // global record index of the chunk's first record
+  const double* cre;
+  int n_out, o0, lane;
+  double acc[4][kNT][2];
+  double bnext[2][kNT];  // B fragments of the next two groups
+
+  __device__ __forceinline__ void loadB(double (&b)[kNT], int64_t grp_rec) const {
+    const double* row = cre + (grp_rec + (lane & 3)) * n_out + o0 + (lane >> 2);
+#pragma unroll
+    for (int n = 0; n < kNT; ++n) b[n] = __ldg(row + 8 * n);
+  }
+  __device__ __forceinline__ void begin(int64_t r0) {
+    rec0 = r0;
+    cnt = 0;
+    loadB(bnext[0], rec0);
+    loadB(bnext[1], rec0 + 4);
+  }
+  __device__ __forceinline__ void flush() {
+    // k-step over the 4 nodes [cnt-4, cnt) held in staging rows 0..3
+    const double* s = reinterpret_cast<const double*>(g_smem + stg);
+    double b[kNT];
+#pragma unroll
+    for (int n = 0; n < kNT; ++n) b[n] = bnext[0][n];
+#pragma unroll
+    for (int n = 0; n < kNT; ++n) bnext[0][n] = bnext[1][n];
+    loadB(bnext[1], rec0 + cnt + 4);
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const double a = s[(lane & 3) * kStride + 8 * m + (lane >> 2)];
+#pragma unroll
+      for (int n = 0; n < kNT; ++n)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+                     : "d"(a), "d"(b[n]));
+    }
+  }
+  __device__ __forceinline__ void push(double re) {
+    reinterpret_cast<double*>(g_smem + stg)[(cnt & 3u) * kStride + lane] = re;
+    ++cnt;
+    if ((cnt & 3u) == 0) flush();
+  }
+  __device__ __forceinline__ void finish() {
+    while (cnt & 3u) push(0.0);
+  }
+};
+
+template <int K, bool HYB>
+__device__ __forceinline__ void leaf_block_mma(const Stream& st, double2 pv, MmaSink& sk,
+                                               const Seeds<double, HYB>& sd) {
+  int4 r[K];
+  double2 s[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
+#pragma unroll
+  for (int j = 0; j < K; ++j) s[j] = sd(rec_off(r[j]));
+#pragma unroll
+  for (int j = 0; j < K; ++j) sk.push(s[j].x * pv.x - s[j].y * pv.y);
+}
+
+template <int D, int NU, bool HYB>
+__device__ __forceinline__ void k2mma_visit(Stream& st, uint32_t n, double2 pv, MmaSink& sk,
+                                            const Seeds<double, HYB>& sd) {
+  if constexpr (D > NU) {
+    return;
+  } else if constexpr (D == NU) {
+    while (n >= 4) {
+      leaf_block_mma<4, HYB>(st, pv, sk, sd);
+      st.advance(4);
+      n -= 4;
+    }
+    switch (n) {
+      case 1: leaf_block_mma<1, HYB>(st, pv, sk, sd); break;
+      case 2: leaf_block_mma<2, HYB>(st, pv, sk, sd); break;
+      case 3: leaf_block_mma<3, HYB>(st, pv, sk, sd); break;
+      default: break;
+    }
+    st.advance(n);
+  } else {
+    for (uint32_t j = 0; j < n; ++j) {
+      const int4 r = st.at(0);
+      st.advance(1);
+      const double2 v = cmul(sd(rec_off(r)), pv);
+      sk.push(v.x);
+      k2mma_visit<D + 1, NU, HYB>(st, rec_nch(r), v, sk, sd);
+    }
+  }
+}
+
+template <int NU, int WARPS, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k2_mma(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
+       int Us, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
+       const double* __restrict__ cre, int n_out, int o0, double* __restrict__ out,
+       double2* __restrict__ gcache, double* __restrict__ part) {
+  constexpr int NOC = 8 * MmaSink::kNT;
+  unsigned char* smem = g_smem;
+  double2* sA = reinterpret_cast<double2*>(smem);
+  const uint32_t rings = (uint32_t)((size_t)Us * 32 * sizeof(double2));
+  const uint32_t stgs = rings + WARPS * 64 * 16;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
+  Seeds<double, HYB> sd;
+  sd.s = (uint32_t)(lane * 16);
+  sd.g = HYB ? reinterpret_cast<const char*>(gA) + lane * 16 - (size_t)Us * 512 : nullptr;
+  sd.us_bytes = (uint32_t)((size_t)Us * 512);
+  const int nc = min(NOC, n_out - o0);
+  double* mypart = part + (size_t)blockIdx.x * WARPS * 32 * NOC;
+  const int4* prog = reinterpret_cast<const int4*>(ops);
+  Stream st;
+  MmaSink sk;
+  sk.stg = stgs + warp * 4 * MmaSink::kStride * 8;
+  sk.cre = cre;
+  sk.n_out = n_out;
+  sk.o0 = o0;
+  sk.lane = lane;
+  const int64_t ntiles = (S + 31) / 32;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    stage_seeds<double2, HYB>(A, S, L, tile, slot_label, U, Us, sA, gA, warp, WARPS, lane);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int n = 0; n < MmaSink::kNT; ++n) sk.acc[m][n][0] = sk.acc[m][n][1] = 0.0;
+    for (int ci = warp; ci < nchunk; ci += WARPS) {
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(prog + b, (uint32_t)(e - b), rings + warp * 64 * 16, lane);
+      sk.begin(b);
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        st.advance(2);
+        const double2 v = cmul(sd(rec_off(r0)), sd(rec_off(r1)));
+        sk.push(v.x);
+        sk.push(0.0);  // the root's second record carries no coefficients
+        k2mma_visit<3, NU, HYB>(st, rec_nch(r0), v, sk, sd);
+      }
+      sk.finish();
+    }
+    // C fragment (m, n): rows = sites 8m + lane/4, cols = outputs 8n + 2(lane%4) + {0,1}
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int n = 0; n < MmaSink::kNT; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int site = 8 * m + (lane >> 2), o = 8 * n + 2 * (lane & 3) + j;
+          mypart[((size_t)warp * 32 + site) * NOC + o] = sk.acc[m][n][j];
+        }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 32 * NOC; idx += WARPS * 32) {
+      const int site_l = idx / NOC, o = idx % NOC;
+      double s = 0.0;
+      for (int w = 0; w < WARPS; ++w) s += __ldcg(mypart + ((size_t)w * 32 + site_l) * NOC + o);
+      const int64_t site = tile * 32 + site_l;
+      if (site < S && o < nc) out[site * n_out + o0 + o] = s;
     }
     __syncthreads();
   }

@@ -163,9 +163,21 @@ struct acedag_plan {
   DevBuf<int32_t> nseg;
   DevBuf<uint16_t> nslots;
   DevBuf<double> ncre, ncim;
-  DevBuf<double2> gcache;
-  DevBuf<double2> ws_A;
-  DevBuf<double> part;  // K2 per-chunk partial sums [grid][chunks][32]
+  // per-stream scratch (seed cold tails, chunk partials, pooled A): calls on
+  // distinct streams may run concurrently
+  struct Workspace {
+    DevBuf<double2> gcache;
+    DevBuf<double2> ws_A;
+    DevBuf<double> part;  // K2 partial sums
+  };
+  std::mutex ws_mu;
+  std::map<void*, std::unique_ptr<Workspace>> wss;
+  Workspace* ws(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(ws_mu);
+    auto& w = wss[(void*)s];
+    if (!w) w.reset(new Workspace);
+    return w.get();
+  }
 };
 
 // ====================================================================== API
@@ -400,6 +412,7 @@ struct Launch {
   int grid, block, us, rows;
   size_t smem;
   bool hyb;
+  acedag_plan::Workspace* ws;
 };
 
 // K2 fast-path geometry: warps per CTA (16 -> 128 registers and 8-leaf
@@ -415,20 +428,21 @@ int k2_warps() {
 
 // tile geometry: 32 sites per CTA, seed rows [Us][32] in smem (U used seeds
 // plus the constant ONE row), the tail in the per-CTA global cache
-int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, int warps, Launch& lc) {
-  const int64_t ntiles = (S + 31) / 32;
+int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, int warps, Launch& lc,
+                int tile = 32) {
+  const int64_t ntiles = (S + tile - 1) / tile;
   lc.block = warps * 32;
   lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
   lc.rows = P->U + 1;
   size_t avail = P->smem_optin > red_bytes ? P->smem_optin - red_bytes : 0;
-  int us_max = (int)(avail / (32 * elem));
+  int us_max = (int)(avail / (tile * elem));
   lc.us = std::min(lc.rows, us_max);
   lc.hyb = lc.us < lc.rows;
-  lc.smem = (size_t)lc.us * 32 * elem + red_bytes;
+  lc.smem = (size_t)lc.us * tile * elem + red_bytes;
   if (lc.hyb) {
     // sized in double2 units; float2 tables use the first half
-    size_t need = (size_t)lc.grid * (lc.rows - lc.us) * 32;
-    if (P->gcache.alloc(need) != cudaSuccess) return fail(ACEDAG_ENOMEM, "gcache allocation failed");
+    size_t need = (size_t)lc.grid * (lc.rows - lc.us) * tile;
+    if (lc.ws->gcache.alloc(need) != cudaSuccess) return fail(ACEDAG_ENOMEM, "gcache allocation failed");
   }
   return 0;
 }
@@ -446,13 +460,42 @@ cudaError_t launch_fast_w(acedag_plan* P, const void* A, int64_t S, int L, const
   auto k = dev::k2_fast<NU, T, WARPS, MAXU, HYB>;
   cudaError_t e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
-  e = P->part.alloc((size_t)lc.grid * nchunks(P) * 32);
+  e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 32);
   if (e != cudaSuccess) return e;
   k<<<lc.grid, lc.block, lc.smem, st>>>(
       reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
-      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(P->gcache.p), P->part.p,
+      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(lc.ws->gcache.p), lc.ws->part.p,
       k2_sched());
   return cudaGetLastError();
+}
+
+// two sites per lane (64-site tiles): ACEDAG_K2_SPL=1 selects the 32-site kernel
+int k2_spl() {
+  static int s = [] {
+    const char* e = getenv("ACEDAG_K2_SPL");
+    return e && atoi(e) == 1 ? 1 : 2;
+  }();
+  return s;
+}
+
+template <int NU, typename T, int WARPS, int MAXU, bool HYB>
+cudaError_t launch_fast2_w(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
+                           double* out, const Launch& lc, cudaStream_t st) {
+  auto k = dev::k2_fast2<NU, T, WARPS, MAXU, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  e = lc.ws->part.alloc((size_t)lc.grid * WARPS * 64);
+  if (e != cudaSuccess) return e;
+  k<<<lc.grid, lc.block, lc.smem, st>>>(
+      reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
+      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(lc.ws->gcache.p), lc.ws->part.p);
+  return cudaGetLastError();
+}
+
+template <int NU, typename T, bool HYB>
+cudaError_t launch_fast2(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
+                         double* out, const Launch& lc, cudaStream_t st) {
+  return launch_fast2_w<NU, T, 32, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
 }
 
 template <int NU, typename T, bool HYB>
@@ -470,11 +513,11 @@ cudaError_t launch_multi(acedag_plan* P, const double2* A, int64_t S, int L, con
   auto k = dev::k2_multi<NU, kMultiWarps, kNOC, HYB>;
   cudaError_t e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
-  e = P->part.alloc((size_t)lc.grid * kMultiWarps * kNOC * 32);
+  e = lc.ws->part.alloc((size_t)lc.grid * kMultiWarps * kNOC * 32);
   if (e != cudaSuccess) return e;
   for (int o0 = 0; o0 < P->host.n_out; o0 += kNOC) {
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                          P->cre.p, P->host.n_out, o0, out, P->gcache.p, P->part.p);
+                                          P->cre.p, P->host.n_out, o0, out, lc.ws->gcache.p, lc.ws->part.p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -489,11 +532,11 @@ cudaError_t launch_mma(acedag_plan* P, const double2* A, int64_t S, int L, const
   auto k = dev::k2_mma<NU, kMmaWarps, HYB>;
   cudaError_t e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
-  e = P->part.alloc((size_t)lc.grid * kMmaWarps * 32 * 32);
+  e = lc.ws->part.alloc((size_t)lc.grid * kMmaWarps * 32 * 32);
   if (e != cudaSuccess) return e;
   for (int o0 = 0; o0 < P->host.n_out; o0 += 32) {
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                          P->cre.p, P->host.n_out, o0, out, P->gcache.p, P->part.p);
+                                          P->cre.p, P->host.n_out, o0, out, lc.ws->gcache.p, lc.ws->part.p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -520,7 +563,7 @@ cudaError_t launch_general(acedag_plan* P, const double2* A, int64_t S, int L,
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p,
                                           nchunks(P), P->cre.p,
                                           P->host.complex_coef ? P->cim.p : nullptr, P->host.n_out, o0,
-                                          complex_out, out, P->gcache.p);
+                                          complex_out, out, lc.ws->gcache.p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -537,7 +580,7 @@ cudaError_t launch_naive(acedag_plan* P, const double2* A, int64_t S, int L,
   for (int o0 = 0; o0 < P->host.n_out; ++o0) {
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->nseg.p, P->nslots.p,
                                           P->ncre.p, P->host.complex_coef ? P->ncim.p : nullptr,
-                                          P->host.n_out, o0, complex_out, out, P->gcache.p);
+                                          P->host.n_out, o0, complex_out, out, lc.ws->gcache.p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -560,6 +603,16 @@ cudaError_t by_order(int nu, Args&&... a) {
 template <int NU> struct FastF64 {
   template <typename... A> static cudaError_t run(bool hyb, A... a) {
     return hyb ? launch_fast<NU, double, true>(a...) : launch_fast<NU, double, false>(a...);
+  }
+};
+template <int NU> struct Fast2F64 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_fast2<NU, double, true>(a...) : launch_fast2<NU, double, false>(a...);
+  }
+};
+template <int NU> struct Fast2F32 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_fast2<NU, float, true>(a...) : launch_fast2<NU, float, false>(a...);
   }
 };
 template <int NU> struct FastF32 {
@@ -598,17 +651,30 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
   const PlanHost& H = P->host;
   const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
   Launch lc;
+  lc.ws = P->ws(st);
   cudaError_t e;
   if (method == ACEDAG_METHOD_RECURSIVE) {
     if (prec == ACEDAG_PREC_F32) {
       if (!fast) return fail(ACEDAG_EUNSUPPORTED, "fp32 mode supports real coefficients, one real output");
-      int rc = plan_launch(P, S, sizeof(float2), k2_warps() * 1024 + 16, k2_warps(), lc);
-      if (rc) return rc;
-      e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+      if (k2_spl() == 2) {
+        int rc = plan_launch(P, S, sizeof(float2), 32 * 1024, 32, lc, 64);
+        if (rc) return rc;
+        e = by_order<Fast2F32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+      } else {
+        int rc = plan_launch(P, S, sizeof(float2), k2_warps() * 1024 + 16, k2_warps(), lc);
+        if (rc) return rc;
+        e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+      }
     } else if (fast) {
-      int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024 + 16, k2_warps(), lc);
-      if (rc) return rc;
-      e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+      if (k2_spl() == 2) {
+        int rc = plan_launch(P, S, sizeof(double2), 32 * 1024, 32, lc, 64);
+        if (rc) return rc;
+        e = by_order<Fast2F64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+      } else {
+        int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024 + 16, k2_warps(), lc);
+        if (rc) return rc;
+        e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+      }
     } else if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out >= 8 && use_mma()) {
       // smem beyond the seed rows: 16 program rings + 16 x [4][36] staging
       int rc = plan_launch(P, S, sizeof(double2), kMmaWarps * 1024 + kMmaWarps * 4 * 36 * 8, kMmaWarps, lc);
@@ -791,16 +857,17 @@ int acedag_eval_from_positions(acedag_plan* P, const double* xyz, const int32_t*
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t chunk = 1 << 17;
   const int U = P->U;
-  if (P->ws_A.alloc((size_t)std::min<int64_t>(S, chunk) * U) != cudaSuccess)
+  acedag_plan::Workspace* W = P->ws(st);
+  if (W->ws_A.alloc((size_t)std::min<int64_t>(S, chunk) * U) != cudaSuccess)
     return fail(ACEDAG_ENOMEM, "workspace allocation failed");
   const int cap = P->g->spec.int_cap();
   const size_t osz = out_kind == ACEDAG_OUT_COMPLEX ? 16 : 8;
   for (int64_t s0 = 0; s0 < S; s0 += chunk) {
     const int64_t n = std::min(chunk, S - s0);
     int rc = pool_positions_impl(cap, xyz + s0 * J * 3, counts ? counts + s0 : nullptr, n, J, r_in, r_cut,
-                                 P->used_labels.p, U, U, reinterpret_cast<double*>(P->ws_A.p), st);
+                                 P->used_labels.p, U, U, reinterpret_cast<double*>(W->ws_A.p), st);
     if (rc) return rc;
-    rc = eval_impl(P, ACEDAG_METHOD_RECURSIVE, ACEDAG_PREC_F64, out_kind, P->ws_A.p, n, U,
+    rc = eval_impl(P, ACEDAG_METHOD_RECURSIVE, ACEDAG_PREC_F64, out_kind, W->ws_A.p, n, U,
                    P->slot_identity.p, static_cast<char*>(out) + s0 * P->host.n_out * osz, st);
     if (rc) return rc;
   }

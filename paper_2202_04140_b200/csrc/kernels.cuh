@@ -304,6 +304,163 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
   }
 }
 
+// ------------------------------------------------------ K2 (two sites/lane)
+// 64-site tiles: lane handles sites t*64 + lane and t*64 + 32 + lane, so each
+// program record (and its decode) serves twice the sites.  The seed table is
+// [slot][64 sites] c128 (1 KB rows); the hottest rows (98% of fetches at
+// cfg2/cfg5) stay in shared memory, the cold tail in the per-CTA global cache.
+template <typename T, bool HYB>
+struct Seeds2 {
+  using V = typename V2<T>::t;
+  static constexpr uint32_t kRow = 64 * sizeof(V);  // bytes per slot row
+  uint32_t s;         // g_smem byte offset of this lane's entry (first half) in row 0
+  const char* g;      // global cache base + lane * sizeof(V) - us_bytes
+  uint32_t us_bytes;  // smem rows * kRow
+  __device__ __forceinline__ void operator()(uint32_t off, V& a, V& b) const {
+    const uint32_t o = (off / kRowBytes) * kRow;  // records carry slot * 512
+    if (!HYB || o < us_bytes) {
+      a = *reinterpret_cast<const V*>(g_smem + s + o);
+      b = *reinterpret_cast<const V*>(g_smem + s + o + 32 * sizeof(V));
+    } else {
+      a = *reinterpret_cast<const V*>(g + o);
+      b = *reinterpret_cast<const V*>(g + o + 32 * sizeof(V));
+    }
+  }
+};
+
+template <int K, typename T, bool HYB>
+__device__ __forceinline__ void leaf_block2(const Stream& st, typename V2<T>::t pa, typename V2<T>::t pb,
+                                            T& acc0, T& acc1, const Seeds2<T, HYB>& sd) {
+  using V = typename V2<T>::t;
+  int4 r[K];
+  V sa[K], sb[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
+#pragma unroll
+  for (int j = 0; j < K; ++j) sd(rec_off(r[j]), sa[j], sb[j]);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const T c = (T)rec_c(r[j]);
+    acc0 += c * (sa[j].x * pa.x - sa[j].y * pa.y);
+    acc1 += c * (sb[j].x * pb.x - sb[j].y * pb.y);
+  }
+}
+
+template <int MAXU, typename T, bool HYB>
+__device__ __forceinline__ void leaves2(Stream& st, uint32_t n, typename V2<T>::t pa, typename V2<T>::t pb,
+                                        T& acc0, T& acc1, const Seeds2<T, HYB>& sd) {
+  while (n >= MAXU) {
+    leaf_block2<MAXU, T, HYB>(st, pa, pb, acc0, acc1, sd);
+    st.advance(MAXU);
+    n -= MAXU;
+  }
+  switch (n) {
+    case 1: leaf_block2<1, T, HYB>(st, pa, pb, acc0, acc1, sd); break;
+    case 2: leaf_block2<2, T, HYB>(st, pa, pb, acc0, acc1, sd); break;
+    case 3: leaf_block2<3, T, HYB>(st, pa, pb, acc0, acc1, sd); break;
+    default: break;
+  }
+  st.advance(n);
+}
+
+template <int D, int NU, int MAXU, typename T, bool HYB>
+__device__ __forceinline__ void k2_visit2(Stream& st, uint32_t n, typename V2<T>::t pa, typename V2<T>::t pb,
+                                          T& acc0, T& acc1, const Seeds2<T, HYB>& sd) {
+  using V = typename V2<T>::t;
+  if constexpr (D > NU) {
+    return;
+  } else if constexpr (D == NU) {
+    leaves2<MAXU, T, HYB>(st, n, pa, pb, acc0, acc1, sd);
+  } else {
+    for (uint32_t j = 0; j < n; ++j) {
+      const int4 r = st.at(0);
+      st.advance(1);
+      V sa, sb;
+      sd(rec_off(r), sa, sb);
+      const V va = cmul(sa, pa), vb = cmul(sb, pb);
+      const T c = (T)rec_c(r);
+      acc0 += c * va.x;
+      acc1 += c * vb.x;
+      k2_visit2<D + 1, NU, MAXU, T, HYB>(st, rec_nch(r), va, vb, acc0, acc1, sd);
+    }
+  }
+}
+
+// stage 64 sites: lane covers sites lane and 32 + lane of the tile
+template <typename V, bool HYB>
+__device__ __forceinline__ void stage_seeds2(const V* __restrict__ A, int64_t S, int L, int64_t tile,
+                                             const uint16_t* __restrict__ slot_label, int U, int Us,
+                                             V* sA, V* gA, int warp, int W, int lane) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t site = tile * 64 + h * 32 + lane;
+    const bool valid = site < S;
+    const V* row = A + (valid ? site : 0) * (int64_t)L;
+    for (int u = warp; u <= U; u += W) {
+      V v;
+      if (u == U) { v.x = 1; v.y = 0; }
+      else if (valid) v = ld_stream(row + __ldg(slot_label + u));
+      else { v.x = 0; v.y = 0; }
+      if (!HYB || u < Us) sA[u * 64 + h * 32 + lane] = v;
+      else gA[(u - Us) * 64 + h * 32 + lane] = v;
+    }
+  }
+}
+
+template <int NU, typename T, int WARPS, int MAXU, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k2_fast2(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
+         const uint16_t* __restrict__ slot_label, int U, int Us, const Op* __restrict__ ops,
+         const int32_t* __restrict__ chunk, int nchunk, double* __restrict__ out,
+         typename V2<T>::t* __restrict__ gcache, double* __restrict__ part) {
+  using V = typename V2<T>::t;
+  unsigned char* smem = g_smem;
+  V* sA = reinterpret_cast<V*>(smem);
+  const uint32_t rings = (uint32_t)((size_t)Us * 64 * sizeof(V));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  V* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 64 : nullptr;
+  Seeds2<T, HYB> sd;
+  sd.s = (uint32_t)(lane * sizeof(V));
+  sd.g = HYB ? reinterpret_cast<const char*>(gA) + lane * sizeof(V) - (size_t)Us * 64 * sizeof(V) : nullptr;
+  sd.us_bytes = (uint32_t)((size_t)Us * 64 * sizeof(V));
+  double* mypart = part + (size_t)blockIdx.x * WARPS * 64;
+  Stream st;
+  const int64_t ntiles = (S + 63) / 64;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    stage_seeds2<V, HYB>(A, S, L, tile, slot_label, U, Us, sA, gA, warp, WARPS, lane);
+    __syncthreads();
+    double wa = 0.0, wb = 0.0;
+    for (int ci = warp; ci < nchunk; ci += WARPS) {
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), rings + warp * 64 * 16, lane);
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        st.advance(2);
+        T acc0 = 0, acc1 = 0;
+        V a0, b0, a1, b1;
+        sd(rec_off(r0), a0, b0);
+        sd(rec_off(r1), a1, b1);
+        const V va = cmul(a0, a1), vb = cmul(b0, b1);
+        const T c = (T)rec_c(r0);
+        acc0 += c * va.x;
+        acc1 += c * vb.x;
+        k2_visit2<3, NU, MAXU, T, HYB>(st, rec_nch(r0), va, vb, acc0, acc1, sd);
+        wa += (double)acc0;
+        wb += (double)acc1;
+      }
+    }
+    mypart[(warp * 2 + 0) * 32 + lane] = wa;
+    mypart[(warp * 2 + 1) * 32 + lane] = wb;
+    __syncthreads();
+    if (warp < 2) {
+      double s = 0.0;
+      for (int w = 0; w < WARPS; ++w) s += __ldcg(mypart + (w * 2 + warp) * 32 + lane);
+      const int64_t site = tile * 64 + warp * 32 + lane;
+      if (site < S) out[site] = s;
+    }
+  }
+}
+
 // ------------------------------------------------------- K2 (multi-output)
 // Real coefficients, Re(phi), n_out outputs (BASELINE cfg5: 64): the c . A
 // epilogue is a dense [sites x nodes] x [nodes x n_out] product, FP64-bound.

@@ -255,3 +255,37 @@ def test_host_pipelines_match_device(cuda, cfg2, golden):
     xyz = torch.from_numpy(golden("positions_cfg3.npz")["xyz"])
     assert torch.equal(plan.evaluate_positions(xyz.to(cuda)).cpu(),
                        plan.evaluate_positions_host(xyz.pin_memory(), chunk=2).clone())
+
+
+@pytest.mark.parametrize("env", [{"ACEDAG_K2_SPL": "1"}, {"ACEDAG_K2_SPL": "1", "ACEDAG_K2_WARPS": "16"},
+                                 {"ACEDAG_SCHED": "1"}, {"ACEDAG_MULTI": "scalar"}])
+def test_kernel_variants_in_subprocess(cuda, env):
+    """The alternative K2 geometries (32-site tiles, 16 warps, dynamic chunk
+    schedule, scalar multi-output) are selected once per process by
+    environment variables; each is checked against the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, "tests")
+import paper_2202_04140_b200 as P
+from oracle import acedag_oracle as O
+from _helpers import phi_gate, seeded_A
+g = P.build_graph(P.Group.O3, P.DegreeSpec(1, 10), 4)
+A = seeded_A(70, g.num_seeds, 3)
+re, im = O.evaluate_nodes(g.parents[:, 0], g.parents[:, 1], A[:5])
+for n_out in (1, 8):
+    C = np.random.default_rng(4).normal(size=(len(g.target_ids), n_out))
+    plan = P.SitePlan(g).set_coefficients(node_ids=g.target_ids, values=C if n_out > 1 else C[:, 0])
+    got = plan.evaluate(torch.from_numpy(A).cuda()).cpu().numpy().reshape(70, n_out)
+    for o in range(n_out):
+        pr, _ = O.model_sum(re, im, g.target_ids, C[:, o])
+        ok, w = phi_gate(got[:5, o], pr, O.energy_scale(re, g.target_ids, C[:, o]))
+        assert ok, (n_out, o, w)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

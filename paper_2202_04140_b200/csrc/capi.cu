@@ -157,6 +157,7 @@ struct acedag_plan {
   int U = 0;
   DevBuf<uint16_t> slot_label, slot_identity;
   DevBuf<int32_t> used_labels;
+  DevBuf<int32_t> col_of;  // label -> seed slot or -1 (pool of used labels only)
   DevBuf<Op> ops;
   DevBuf<int32_t> chunk;
   DevBuf<double> cre, cim;
@@ -342,6 +343,11 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   CK(P->slot_label.upload(H.slot_label));
   CK(P->slot_identity.upload(ident));
   CK(P->used_labels.upload(used));
+  {
+    std::vector<int32_t> col((size_t)P->g->n_seeds(), -1);
+    for (int i = 0; i < P->U; ++i) col[H.slot_label[i]] = i;
+    CK(P->col_of.upload(col));
+  }
   CK(P->ops.upload(H.ops));
   CK(P->chunk.upload(H.chunk));
   {
@@ -811,8 +817,9 @@ int acedag_pool(int group, int cap, const double* coords, const int32_t* counts,
   return ACEDAG_OK;
 }
 
+// col_of: label -> output column (or -1), NULL = every label at its index
 static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts, int64_t S, int J,
-                               double r_in, double r_cut, const int32_t* out_labels, int L_out,
+                               double r_in, double r_cut, const int32_t* col_of, int L_out,
                                int64_t out_stride, double* A_out, cudaStream_t st) {
   if (cap < 0 || cap > ACEDAG_YLM_LMAX) return fail(ACEDAG_EUNSUPPORTED, "degree cap outside [0, 40]");
   if (!(r_cut > r_in) || !(r_in >= 0.0)) return fail(ACEDAG_EINVAL, "need 0 <= r_in < r_cut");
@@ -824,16 +831,27 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
   if (rc) return rc;
   const int L = (int)one_particle_indices(kO3, cap).size();
   if (S == 0) return ACEDAG_OK;
-  const size_t smem = (size_t)std::max(J, 1) * dev::pos_stride(cap) * sizeof(double);
+  const size_t smem = dev::pool2_smem(cap, std::max(J, 1));
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   if (smem > (size_t)optin) return fail(ACEDAG_EUNSUPPORTED, "too many neighbours per site for the pool tables");
-  CK(cudaFuncSetAttribute(dev::pool_positions, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int grid = (int)std::min<int64_t>(S, 148 * 8);
-  dev::pool_positions<<<grid, 128, smem, st>>>(xyz, counts, S, J, cap, r_in, r_cut, labels, L,
-                                               out_labels, out_labels ? L_out : L,
-                                               out_labels ? out_stride : L,
-                                               reinterpret_cast<double2*>(A_out));
+  const int64_t stride = col_of ? out_stride : L;
+  double2* out = reinterpret_cast<double2*>(A_out);
+  int sms = 148;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = (int)std::min<int64_t>(S, (int64_t)sms * 16);
+#define ACEDAG_POOL2(CM)                                                                              \
+  do {                                                                                                \
+    CK(cudaFuncSetAttribute(dev::pool_positions2<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    dev::pool_positions2<CM><<<grid, 128, smem, st>>>(xyz, counts, S, J, cap, r_in, r_cut, col_of, stride, out); \
+  } while (0)
+  if (cap <= 8) ACEDAG_POOL2(8);
+  else if (cap <= 12) ACEDAG_POOL2(12);
+  else if (cap <= 16) ACEDAG_POOL2(16);
+  else ACEDAG_POOL2(40);
+#undef ACEDAG_POOL2
+  (void)labels;
+  (void)L_out;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pool_positions");
   return ACEDAG_OK;
@@ -865,7 +883,7 @@ int acedag_eval_from_positions(acedag_plan* P, const double* xyz, const int32_t*
   for (int64_t s0 = 0; s0 < S; s0 += chunk) {
     const int64_t n = std::min(chunk, S - s0);
     int rc = pool_positions_impl(cap, xyz + s0 * J * 3, counts ? counts + s0 : nullptr, n, J, r_in, r_cut,
-                                 P->used_labels.p, U, U, reinterpret_cast<double*>(W->ws_A.p), st);
+                                 P->col_of.p, U, U, reinterpret_cast<double*>(W->ws_A.p), st);
     if (rc) return rc;
     rc = eval_impl(P, ACEDAG_METHOD_RECURSIVE, ACEDAG_PREC_F64, out_kind, W->ws_A.p, n, U,
                    P->slot_identity.p, static_cast<char*>(out) + s0 * P->host.n_out * osz, st);

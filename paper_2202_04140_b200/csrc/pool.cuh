@@ -201,3 +201,128 @@ __global__ void pool_positions(const double* __restrict__ xyz, const int32_t* __
 
 }  // namespace dev
 }  // namespace acedag
+
+namespace acedag {
+namespace dev {
+
+// ------------------------------------------------------- positions, v2
+// One CTA per site (grid-stride).  Phase A: per neighbour the weighted radial
+// row WR[j][n] = f_c(r_j) T_n(2x_j - 1) and the direction (cos t, sin t,
+// e^{i phi}).  Phase B: per (neighbour, m) the normalised Legendre column and
+// Y[j][l(l+1)/2 + m] = Nbar_lm P_l^m e^{i m phi} for m >= 0.  Phase C: one
+// thread per (l, m >= 0) accumulates A[n, l, m] = sum_j WR[j][n] Y[j][lm] for
+// every n in registers; A[n, l, -m] = (-1)^m conj(A[n, l, m]) (real weights),
+// so only half of the labels are computed.  col_of maps a label to its output
+// column (-1: not needed); NULL writes every label at its own index.
+template <int CAPMAX>
+__global__ void __launch_bounds__(128)
+pool_positions2(const double* __restrict__ xyz, const int32_t* __restrict__ counts, int64_t S, int J,
+                int cap, double r_in, double r_cut, const int32_t* __restrict__ col_of,
+                int64_t out_stride, double2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  const int npair = (cap + 1) * (cap + 2) / 2;
+  double2* Y = reinterpret_cast<double2*>(psm);                  // [J][npair]
+  double* WR = reinterpret_cast<double*>(Y + (size_t)J * npair);   // [J][cap+1]
+  double* G = WR + (size_t)J * (cap + 1);                         // [J][4]
+  const double inv_span = 1.0 / (r_cut - r_in);
+  for (int64_t s = blockIdx.x; s < S; s += gridDim.x) {
+    const int nj = counts ? min(counts[s], J) : J;
+    for (int j = threadIdx.x; j < nj; j += blockDim.x) {
+      const double* p = xyz + (s * J + j) * 3;
+      const double x = p[0], y = p[1], z = p[2];
+      const double rho2 = x * x + y * y;
+      const double r = sqrt(rho2 + z * z);
+      const double w = r < r_cut ? 0.5 * (1.0 + cospi(r / r_cut)) : 0.0;
+      const double u = 2.0 * fmin(1.0, fmax(0.0, (r - r_in) * inv_span)) - 1.0;
+      double* wr = WR + j * (cap + 1);
+      double t0 = 1.0, t1 = u;
+      wr[0] = w;
+      if (cap >= 1) wr[1] = w * u;
+      for (int n = 2; n <= cap; ++n) {
+        const double t2 = 2.0 * u * t1 - t0;
+        wr[n] = w * t2;
+        t0 = t1;
+        t1 = t2;
+      }
+      const double rho = sqrt(rho2);
+      G[4 * j + 0] = r > 0.0 ? z / r : 1.0;     // cos theta
+      G[4 * j + 1] = r > 0.0 ? rho / r : 0.0;   // sin theta
+      G[4 * j + 2] = rho > 0.0 ? x / rho : 1.0; // cos phi
+      G[4 * j + 3] = rho > 0.0 ? y / rho : 0.0; // sin phi
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nj * (cap + 1); idx += blockDim.x) {
+      const int j = idx / (cap + 1), m = idx - j * (cap + 1);
+      const double4 g = make_double4(G[4 * j], G[4 * j + 1], G[4 * j + 2], G[4 * j + 3]);
+      double ec = 1.0, es = 0.0;  // e^{i m phi}
+      for (int k = 0; k < m; ++k) {
+        const double nc = ec * g.z - es * g.w;
+        es = ec * g.w + es * g.z;
+        ec = nc;
+      }
+      double pmm = 1.0;
+      for (int k = 1; k <= m; ++k) pmm *= -(2.0 * k - 1.0) * g.y;
+      double2* yj = Y + (size_t)j * npair;
+      double nv = c_ylm_norm[m * (m + 1) / 2 + m] * pmm;
+      yj[m * (m + 1) / 2 + m] = make_double2(nv * ec, nv * es);
+      if (m + 1 <= cap) {
+        double p0 = pmm, p1 = g.x * (2.0 * m + 1.0) * pmm;
+        nv = c_ylm_norm[(m + 1) * (m + 2) / 2 + m] * p1;
+        yj[(m + 1) * (m + 2) / 2 + m] = make_double2(nv * ec, nv * es);
+        for (int l = m + 2; l <= cap; ++l) {
+          const double p2 = (g.x * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) / (double)(l - m);
+          nv = c_ylm_norm[l * (l + 1) / 2 + m] * p2;
+          yj[l * (l + 1) / 2 + m] = make_double2(nv * ec, nv * es);
+          p0 = p1;
+          p1 = p2;
+        }
+      }
+    }
+    __syncthreads();
+    for (int pair = threadIdx.x; pair < npair; pair += blockDim.x) {
+      int l = 0;
+      while ((l + 1) * (l + 2) / 2 <= pair) ++l;
+      const int m = pair - l * (l + 1) / 2;
+      const int nmax = cap - l;
+      double2 acc[CAPMAX + 1];
+#pragma unroll
+      for (int n = 0; n <= CAPMAX; ++n) acc[n] = make_double2(0.0, 0.0);
+      for (int j = 0; j < nj; ++j) {
+        const double2 yv = Y[(size_t)j * npair + pair];
+        const double* wr = WR + j * (cap + 1);
+#pragma unroll
+        for (int n = 0; n <= CAPMAX; ++n)
+          if (n <= nmax) {
+            const double a = wr[n];
+            acc[n].x += a * yv.x;
+            acc[n].y += a * yv.y;
+          }
+      }
+      // label index of (n, l, m): n-blocks of (cap-n'+1)^2 labels, then l^2 + (m + l)
+      int base = 0;
+#pragma unroll
+      for (int n = 0; n <= CAPMAX; ++n) {
+        if (n <= nmax) {
+          const int lab_p = base + l * l + (m + l), lab_m = base + l * l + (l - m);
+          const int cp = col_of ? col_of[lab_p] : lab_p;
+          if (cp >= 0) out[s * out_stride + cp] = acc[n];
+          if (m > 0) {
+            const int cm = col_of ? col_of[lab_m] : lab_m;
+            const double sg = (m & 1) ? -1.0 : 1.0;
+            if (cm >= 0) out[s * out_stride + cm] = make_double2(sg * acc[n].x, -sg * acc[n].y);
+          }
+        }
+        base += (cap - n + 1) * (cap - n + 1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+inline size_t pool2_smem(int cap, int J) {
+  const size_t npair = (size_t)(cap + 1) * (cap + 2) / 2;
+  return (size_t)J * npair * 16 + (size_t)J * (cap + 1) * 8 + (size_t)J * 32;
+}
+
+}  // namespace dev
+}  // namespace acedag

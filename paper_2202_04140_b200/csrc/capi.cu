@@ -97,6 +97,10 @@ int ensure_norms(int dev) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (g_norms_ready[dev]) return 0;
   CK(cudaMemcpyToSymbol(dev::c_ylm_norm, kYlmNorm, sizeof(kYlmNorm)));
+  double recip[ACEDAG_YLM_LMAX + 2];
+  recip[0] = 0.0;
+  for (int k = 1; k < ACEDAG_YLM_LMAX + 2; ++k) recip[k] = 1.0 / k;
+  CK(cudaMemcpyToSymbol(dev::c_recip, recip, sizeof(recip)));
   g_norms_ready[dev] = true;
   return 0;
 }

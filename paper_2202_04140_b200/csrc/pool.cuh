@@ -21,6 +21,7 @@ namespace acedag {
 namespace dev {
 
 __constant__ double c_ylm_norm[(ACEDAG_YLM_LMAX + 1) * (ACEDAG_YLM_LMAX + 2) / 2];
+__constant__ double c_recip[ACEDAG_YLM_LMAX + 2];  // 1/k, k = 0..LMAX+1 (entry 0 unused)
 
 __device__ __forceinline__ double cheb_exact(int k, double x) {  // special.py:19-28
   if (k == 0) return 1.0;
@@ -270,7 +271,7 @@ pool_positions2(const double* __restrict__ xyz, const int32_t* __restrict__ coun
         nv = c_ylm_norm[(m + 1) * (m + 2) / 2 + m] * p1;
         yj[(m + 1) * (m + 2) / 2 + m] = make_double2(nv * ec, nv * es);
         for (int l = m + 2; l <= cap; ++l) {
-          const double p2 = (g.x * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) / (double)(l - m);
+          const double p2 = (g.x * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) * c_recip[l - m];
           nv = c_ylm_norm[l * (l + 1) / 2 + m] * p2;
           yj[l * (l + 1) / 2 + m] = make_double2(nv * ec, nv * es);
           p0 = p1;

@@ -502,9 +502,26 @@ cudaError_t launch_fast2_w(acedag_plan* P, const void* A, int64_t S, int L, cons
   return cudaGetLastError();
 }
 
+// leaf batch of the two-site kernel (ACEDAG_K2_MAXU = 2 or 4)
+int k2_maxu() {
+  static int m = [] {
+    const char* e = getenv("ACEDAG_K2_MAXU");
+    return e && atoi(e) == 2 ? 2 : 4;
+  }();
+  return m;
+}
+
 template <int NU, typename T, bool HYB>
 cudaError_t launch_fast2(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
                          double* out, const Launch& lc, cudaStream_t st) {
+  const int w = lc.block / 32;
+  if (k2_maxu() == 2) {
+    if (w == 16) return launch_fast2_w<NU, T, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+    if (w == 24) return launch_fast2_w<NU, T, 24, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+    return launch_fast2_w<NU, T, 32, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+  }
+  if (w == 16) return launch_fast2_w<NU, T, 16, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
+  if (w == 24) return launch_fast2_w<NU, T, 24, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
   return launch_fast2_w<NU, T, 32, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
 }
 
@@ -667,7 +684,7 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
     if (prec == ACEDAG_PREC_F32) {
       if (!fast) return fail(ACEDAG_EUNSUPPORTED, "fp32 mode supports real coefficients, one real output");
       if (k2_spl() == 2) {
-        int rc = plan_launch(P, S, sizeof(float2), 32 * 1024, 32, lc, 64);
+        int rc = plan_launch(P, S, sizeof(float2), k2_warps() * 1024, k2_warps(), lc, 64);
         if (rc) return rc;
         e = by_order<Fast2F32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
       } else {
@@ -677,7 +694,7 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
       }
     } else if (fast) {
       if (k2_spl() == 2) {
-        int rc = plan_launch(P, S, sizeof(double2), 32 * 1024, 32, lc, 64);
+        int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024, k2_warps(), lc, 64);
         if (rc) return rc;
         e = by_order<Fast2F64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
       } else {

@@ -356,8 +356,8 @@ __device__ __forceinline__ void leaves2(Stream& st, uint32_t n, typename V2<T>::
   }
   switch (n) {
     case 1: leaf_block2<1, T, HYB>(st, pa, pb, acc0, acc1, sd); break;
-    case 2: leaf_block2<2, T, HYB>(st, pa, pb, acc0, acc1, sd); break;
-    case 3: leaf_block2<3, T, HYB>(st, pa, pb, acc0, acc1, sd); break;
+    case 2: if constexpr (MAXU > 2) leaf_block2<2, T, HYB>(st, pa, pb, acc0, acc1, sd); break;
+    case 3: if constexpr (MAXU > 3) leaf_block2<3, T, HYB>(st, pa, pb, acc0, acc1, sd); break;
     default: break;
   }
   st.advance(n);

@@ -289,3 +289,22 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("group,p,D,nu,alg,n", [
+    ("T", 1, 10, 5, "orig", 1), ("SO2", 1, 7, 4, "gen", 2), ("O3", 2, 4, 4, "orig", 1),
+    ("O3", math.inf, 3, 3, "gen", 3), ("O3F", 1, 5, 4, "orig", 1), ("O3", 1, 9, 6, "orig", 1)])
+def test_all_groups_and_specs_through_k2_k3(cuda, group, p, D, nu, alg, n):
+    """K2/K3 are group-agnostic: every group, p-norm and insertion rule."""
+    g = P.build_graph(P.Group(group), P.DegreeSpec(p, D), nu, alg, n)
+    S = 37
+    A = seeded_A(S, g.num_seeds, D * 10 + nu)
+    c = np.random.default_rng(nu).normal(size=len(g.target_ids))
+    plan = P.SitePlan(g).set_coefficients(node_ids=g.target_ids, values=c)
+    At = torch.from_numpy(A).to(cuda)
+    pr, _, scale = _oracle_phi(g, A, g.target_ids, c)
+    for method in ("recursive", "naive"):
+        ok, worst = phi_gate(plan.evaluate(At, method=method).cpu().numpy(), pr, scale)
+        assert ok, (method, worst)
+    ok, worst = phi_gate(plan.evaluate(At.to(torch.complex64)).cpu().numpy(), pr, scale, tol=1e-5)
+    assert ok, ("fp32", worst)

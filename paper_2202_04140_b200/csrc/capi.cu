@@ -138,6 +138,36 @@ int plan_chunks() {
   return c;
 }
 
+// (n, l, m >= 0) triples of the O3 labels with cap, keeping those for which
+// keep(label) or keep(label of -m) holds; int4 (n, l, m, label index)
+template <class Keep>
+std::vector<int4> triples(int cap, Keep keep) {
+  std::vector<int4> tri;
+  int lab = 0;
+  for (int n = 0; n <= cap; ++n)
+    for (int l = 0; l <= cap - n; ++l)
+      for (int m = -l; m <= l; ++m, ++lab)
+        if (m >= 0 && (keep(lab) || keep(lab - 2 * m))) tri.push_back(make_int4(n, l, m, lab));
+  return tri;
+}
+
+int full_triples(int dev, int cap, const int4** out, int* n) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  static std::map<std::pair<int, int>, std::pair<int4*, int>> cache;
+  auto key = std::make_pair(dev, cap);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    std::vector<int4> tri = triples(cap, [](int) { return true; });
+    int4* d = nullptr;
+    CK(cudaMalloc(&d, std::max<size_t>(1, tri.size()) * sizeof(int4)));
+    CK(cudaMemcpy(d, tri.data(), tri.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    it = cache.emplace(key, std::make_pair(d, (int)tri.size())).first;
+  }
+  *out = it->second.first;
+  *n = it->second.second;
+  return 0;
+}
+
 int current_device() {
   int d = 0;
   cudaGetDevice(&d);
@@ -162,6 +192,7 @@ struct acedag_plan {
   DevBuf<uint16_t> slot_label, slot_identity;
   DevBuf<int32_t> used_labels;
   DevBuf<int32_t> col_of;  // label -> seed slot or -1 (pool of used labels only)
+  DevBuf<int4> tri;        // (n, l, m >= 0) triples the used labels need
   DevBuf<Op> ops;
   DevBuf<int32_t> chunk;
   DevBuf<double> cre, cim;
@@ -351,6 +382,10 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
     std::vector<int32_t> col((size_t)P->g->n_seeds(), -1);
     for (int i = 0; i < P->U; ++i) col[H.slot_label[i]] = i;
     CK(P->col_of.upload(col));
+    if (P->g->group == kO3) {
+      std::vector<int4> tri = triples(P->g->spec.int_cap(), [&](int lab) { return col[lab] >= 0; });
+      CK(P->tri.upload(tri));
+    }
   }
   CK(P->ops.upload(H.ops));
   CK(P->chunk.upload(H.chunk));
@@ -838,10 +873,11 @@ int acedag_pool(int group, int cap, const double* coords, const int32_t* counts,
   return ACEDAG_OK;
 }
 
-// col_of: label -> output column (or -1), NULL = every label at its index
+// col_of: label -> output column (or -1), NULL = every label at its index;
+// tri/ntri: the triples to compute (NULL = all of this cap)
 static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts, int64_t S, int J,
-                               double r_in, double r_cut, const int32_t* col_of, int L_out,
-                               int64_t out_stride, double* A_out, cudaStream_t st) {
+                               double r_in, double r_cut, const int32_t* col_of, const int4* tri,
+                               int ntri, int64_t out_stride, double* A_out, cudaStream_t st) {
   if (cap < 0 || cap > ACEDAG_YLM_LMAX) return fail(ACEDAG_EUNSUPPORTED, "degree cap outside [0, 40]");
   if (!(r_cut > r_in) || !(r_in >= 0.0)) return fail(ACEDAG_EINVAL, "need 0 <= r_in < r_cut");
   const int dev = current_device();
@@ -861,18 +897,14 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = (int)std::min<int64_t>(S, (int64_t)sms * 16);
-#define ACEDAG_POOL2(CM)                                                                              \
-  do {                                                                                                \
-    CK(cudaFuncSetAttribute(dev::pool_positions2<CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    dev::pool_positions2<CM><<<grid, 128, smem, st>>>(xyz, counts, S, J, cap, r_in, r_cut, col_of, stride, out); \
-  } while (0)
-  if (cap <= 8) ACEDAG_POOL2(8);
-  else if (cap <= 12) ACEDAG_POOL2(12);
-  else if (cap <= 16) ACEDAG_POOL2(16);
-  else ACEDAG_POOL2(40);
-#undef ACEDAG_POOL2
+  if (!tri) {  // every label: the cached full triple table of this cap
+    int rc2 = full_triples(dev, cap, &tri, &ntri);
+    if (rc2) return rc2;
+  }
+  CK(cudaFuncSetAttribute(dev::pool_positions2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dev::pool_positions2<<<grid, 256, smem, st>>>(xyz, counts, S, J, cap, r_in, r_cut, tri, ntri, col_of,
+                                                stride, out);
   (void)labels;
-  (void)L_out;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pool_positions");
   return ACEDAG_OK;
@@ -881,7 +913,7 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
 int acedag_pool_positions(int cap, const double* xyz, const int32_t* counts, int64_t S, int32_t J,
                           double r_in, double r_cut, double* A_out, void* stream) {
   if (S < 0 || J < 0 || !A_out || (S > 0 && J > 0 && !xyz)) return fail(ACEDAG_EINVAL, "bad pool arguments");
-  return pool_positions_impl(cap, xyz, counts, S, J, r_in, r_cut, nullptr, 0, 0, A_out,
+  return pool_positions_impl(cap, xyz, counts, S, J, r_in, r_cut, nullptr, nullptr, 0, 0, A_out,
                              (cudaStream_t)stream);
 }
 
@@ -904,7 +936,7 @@ int acedag_eval_from_positions(acedag_plan* P, const double* xyz, const int32_t*
   for (int64_t s0 = 0; s0 < S; s0 += chunk) {
     const int64_t n = std::min(chunk, S - s0);
     int rc = pool_positions_impl(cap, xyz + s0 * J * 3, counts ? counts + s0 : nullptr, n, J, r_in, r_cut,
-                                 P->col_of.p, U, U, reinterpret_cast<double*>(W->ws_A.p), st);
+                                 P->col_of.p, P->tri.p, (int)P->tri.n, U, reinterpret_cast<double*>(W->ws_A.p), st);
     if (rc) return rc;
     rc = eval_impl(P, ACEDAG_METHOD_RECURSIVE, ACEDAG_PREC_F64, out_kind, W->ws_A.p, n, U,
                    P->slot_identity.p, static_cast<char*>(out) + s0 * P->host.n_out * osz, st);

@@ -212,14 +212,15 @@ namespace dev {
 // e^{i phi}).  Phase B: per (neighbour, m) the normalised Legendre column and
 // Y[j][l(l+1)/2 + m] = Nbar_lm P_l^m e^{i m phi} for m >= 0.  Phase C: one
 // thread per (l, m >= 0) accumulates A[n, l, m] = sum_j WR[j][n] Y[j][lm] for
-// every n in registers; A[n, l, -m] = (-1)^m conj(A[n, l, m]) (real weights),
-// so only half of the labels are computed.  col_of maps a label to its output
-// column (-1: not needed); NULL writes every label at its own index.
-template <int CAPMAX>
-__global__ void __launch_bounds__(128)
+// Phase C: one thread per (n, l, m >= 0) triple (tri table, only the triples
+// some output needs) accumulates A[n, l, m] = sum_j WR[j][n] Y[j][lm];
+// A[n, l, -m] = (-1)^m conj(A[n, l, m]) (real weights), so only half of the
+// labels are computed.  col_of maps a label to its output column (-1: not
+// needed); NULL writes every label at its own index.
+__global__ void __launch_bounds__(256)
 pool_positions2(const double* __restrict__ xyz, const int32_t* __restrict__ counts, int64_t S, int J,
-                int cap, double r_in, double r_cut, const int32_t* __restrict__ col_of,
-                int64_t out_stride, double2* __restrict__ out) {
+                int cap, double r_in, double r_cut, const int4* __restrict__ tri, int ntri,
+                const int32_t* __restrict__ col_of, int64_t out_stride, double2* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char psm[];
   const int npair = (cap + 1) * (cap + 2) / 2;
   double2* Y = reinterpret_cast<double2*>(psm);                  // [J][npair]
@@ -280,40 +281,24 @@ pool_positions2(const double* __restrict__ xyz, const int32_t* __restrict__ coun
       }
     }
     __syncthreads();
-    for (int pair = threadIdx.x; pair < npair; pair += blockDim.x) {
-      int l = 0;
-      while ((l + 1) * (l + 2) / 2 <= pair) ++l;
-      const int m = pair - l * (l + 1) / 2;
-      const int nmax = cap - l;
-      double2 acc[CAPMAX + 1];
-#pragma unroll
-      for (int n = 0; n <= CAPMAX; ++n) acc[n] = make_double2(0.0, 0.0);
+    // phase C: one thread per (n, l, m >= 0) triple of the table
+    for (int t = threadIdx.x; t < ntri; t += blockDim.x) {
+      const int4 q = __ldg(tri + t);  // (n, l, m, label index of (n, l, m))
+      const int pair = q.y * (q.y + 1) / 2 + q.z;
+      double ar = 0.0, ai = 0.0;
       for (int j = 0; j < nj; ++j) {
         const double2 yv = Y[(size_t)j * npair + pair];
-        const double* wr = WR + j * (cap + 1);
-#pragma unroll
-        for (int n = 0; n <= CAPMAX; ++n)
-          if (n <= nmax) {
-            const double a = wr[n];
-            acc[n].x += a * yv.x;
-            acc[n].y += a * yv.y;
-          }
+        const double a = WR[j * (cap + 1) + q.x];
+        ar += a * yv.x;
+        ai += a * yv.y;
       }
-      // label index of (n, l, m): n-blocks of (cap-n'+1)^2 labels, then l^2 + (m + l)
-      int base = 0;
-#pragma unroll
-      for (int n = 0; n <= CAPMAX; ++n) {
-        if (n <= nmax) {
-          const int lab_p = base + l * l + (m + l), lab_m = base + l * l + (l - m);
-          const int cp = col_of ? col_of[lab_p] : lab_p;
-          if (cp >= 0) out[s * out_stride + cp] = acc[n];
-          if (m > 0) {
-            const int cm = col_of ? col_of[lab_m] : lab_m;
-            const double sg = (m & 1) ? -1.0 : 1.0;
-            if (cm >= 0) out[s * out_stride + cm] = make_double2(sg * acc[n].x, -sg * acc[n].y);
-          }
-        }
-        base += (cap - n + 1) * (cap - n + 1);
+      const int cp = col_of ? col_of[q.w] : q.w;
+      if (cp >= 0) out[s * out_stride + cp] = make_double2(ar, ai);
+      if (q.z > 0) {  // A[n, l, -m] = (-1)^m conj(A[n, l, m])
+        const int lab_m = q.w - 2 * q.z;
+        const int cm = col_of ? col_of[lab_m] : lab_m;
+        const double sg = (q.z & 1) ? -1.0 : 1.0;
+        if (cm >= 0) out[s * out_stride + cm] = make_double2(sg * ar, -sg * ai);
       }
     }
     __syncthreads();

@@ -738,8 +738,8 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
         e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
       }
     } else if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out >= 8 && use_mma()) {
-      // smem beyond the seed rows: 16 program rings + 16 x [4][36] staging
-      int rc = plan_launch(P, S, sizeof(double2), kMmaWarps * 1024 + kMmaWarps * 4 * 36 * 8, kMmaWarps, lc);
+      // smem beyond the seed rows: 16 program rings + 16 x [8][36] staging
+      int rc = plan_launch(P, S, sizeof(double2), kMmaWarps * 1024 + kMmaWarps * 8 * 36 * 8, kMmaWarps, lc);
       if (rc) return rc;
       e = by_order<Mma>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
     } else if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out % 2 == 0) {

@@ -561,15 +561,16 @@ k2_multi(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
 // Real coefficients, n_out outputs: the epilogue sum_k c[k][o] Re(v_k) is a
 // dense [32 sites x nodes] x [nodes x n_out] GEMM per tile, issued on the
 // FP64 tensor cores (mma.sync m8n8k4 f64).  Each warp stages the real parts
-// of its last 4 nodes in shared memory ([4][36] doubles, lane = site); every
+// of its last 8 nodes in shared memory ([8][36] doubles, lane = site); every
 // 4 nodes one k-step of 4 (sites) x 4 (outputs) m8n8k4 tiles accumulates
 // into registers.  Coefficient fragments are prefetched two groups ahead.
 struct MmaSink {
-  static constexpr int kNT = 4;     // n-tiles per pass (32 outputs)
+  static constexpr int kNT = 4;       // n-tiles per pass (32 outputs)
   static constexpr int kStride = 36;  // doubles per staged node row (bank spread)
-  uint32_t stg;     // g_smem byte offset of this warp's [8][kStride] staging
-  uint32_t cnt;     // nodes pushed in the current chunk
-  int64_t rec0;     // global record index of the chunk's first record
+  uint32_t stg;      // g_smem byte offset of this warp's [8][kStride] staging ring
+  uint32_t cnt;      // nodes stored in the current chunk
+  uint32_t done;     // nodes already multiplied in (multiple of 4)
+  int64_t rec0;      // global record index of the chunk's first record
   const double* cre;
   int n_out, o0, lane;
   double acc[4][kNT][2];
@@ -582,19 +583,27 @@ struct MmaSink {
   }
   __device__ __forceinline__ void begin(int64_t r0) {
     rec0 = r0;
-    cnt = 0;
+    cnt = done = 0;
     loadB(bnext[0], rec0);
     loadB(bnext[1], rec0 + 4);
   }
-  __device__ __forceinline__ void flush() {
-    // k-step over the 4 nodes [cnt-4, cnt) held in staging rows 0..3
-    const double* s = reinterpret_cast<const double*>(g_smem + stg);
+  __device__ __forceinline__ void store(double re) {
+    reinterpret_cast<double*>(g_smem + stg)[(cnt & 7u) * kStride + lane] = re;
+    ++cnt;
+  }
+  // one k-step (4 nodes) once four unflushed nodes are staged; callers store
+  // at most 4 nodes between calls, so at most one group is ever pending
+  __device__ __forceinline__ void flush_ready() {
+    if (cnt - done < 4) return;
+    const double* s = reinterpret_cast<const double*>(g_smem + stg) + (done & 4u) * kStride;
     double b[kNT];
 #pragma unroll
-    for (int n = 0; n < kNT; ++n) b[n] = bnext[0][n];
-#pragma unroll
-    for (int n = 0; n < kNT; ++n) bnext[0][n] = bnext[1][n];
-    loadB(bnext[1], rec0 + cnt + 4);
+    for (int n = 0; n < kNT; ++n) {
+      b[n] = bnext[0][n];
+      bnext[0][n] = bnext[1][n];
+    }
+    loadB(bnext[1], rec0 + done + 8);
+    done += 4;
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -606,13 +615,9 @@ struct MmaSink {
                      : "d"(a), "d"(b[n]));
     }
   }
-  __device__ __forceinline__ void push(double re) {
-    reinterpret_cast<double*>(g_smem + stg)[(cnt & 3u) * kStride + lane] = re;
-    ++cnt;
-    if ((cnt & 3u) == 0) flush();
-  }
   __device__ __forceinline__ void finish() {
-    while (cnt & 3u) push(0.0);
+    while (cnt & 3u) store(0.0);
+    flush_ready();
   }
 };
 
@@ -626,7 +631,7 @@ __device__ __forceinline__ void leaf_block_mma(const Stream& st, double2 pv, Mma
 #pragma unroll
   for (int j = 0; j < K; ++j) s[j] = sd(rec_off(r[j]));
 #pragma unroll
-  for (int j = 0; j < K; ++j) sk.push(s[j].x * pv.x - s[j].y * pv.y);
+  for (int j = 0; j < K; ++j) sk.store(s[j].x * pv.x - s[j].y * pv.y);
 }
 
 template <int D, int NU, bool HYB>
@@ -639,6 +644,7 @@ __device__ __forceinline__ void k2mma_visit(Stream& st, uint32_t n, double2 pv, 
       leaf_block_mma<4, HYB>(st, pv, sk, sd);
       st.advance(4);
       n -= 4;
+      sk.flush_ready();
     }
     switch (n) {
       case 1: leaf_block_mma<1, HYB>(st, pv, sk, sd); break;
@@ -647,12 +653,14 @@ __device__ __forceinline__ void k2mma_visit(Stream& st, uint32_t n, double2 pv, 
       default: break;
     }
     st.advance(n);
+    sk.flush_ready();
   } else {
     for (uint32_t j = 0; j < n; ++j) {
       const int4 r = st.at(0);
       st.advance(1);
       const double2 v = cmul(sd(rec_off(r)), pv);
-      sk.push(v.x);
+      sk.store(v.x);
+      sk.flush_ready();
       k2mma_visit<D + 1, NU, HYB>(st, rec_nch(r), v, sk, sd);
     }
   }
@@ -680,7 +688,7 @@ k2_mma(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restri
   const int4* prog = reinterpret_cast<const int4*>(ops);
   Stream st;
   MmaSink sk;
-  sk.stg = stgs + warp * 4 * MmaSink::kStride * 8;
+  sk.stg = stgs + warp * 8 * MmaSink::kStride * 8;
   sk.cre = cre;
   sk.n_out = n_out;
   sk.o0 = o0;
@@ -701,8 +709,9 @@ k2_mma(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restri
         const int4 r0 = st.at(0), r1 = st.at(1);
         st.advance(2);
         const double2 v = cmul(sd(rec_off(r0)), sd(rec_off(r1)));
-        sk.push(v.x);
-        sk.push(0.0);  // the root's second record carries no coefficients
+        sk.store(v.x);
+        sk.store(0.0);  // the root's second record carries no coefficients
+        sk.flush_ready();
         k2mma_visit<3, NU, HYB>(st, rec_nch(r0), v, sk, sd);
       }
       sk.finish();

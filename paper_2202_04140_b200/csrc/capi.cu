@@ -515,13 +515,12 @@ cudaError_t launch_fast_w(acedag_plan* P, const void* A, int64_t S, int L, const
 }
 
 // two sites per lane (64-site tiles): ACEDAG_K2_SPL=1 selects the 32-site kernel
-int k2_spl() {
-  static int s = [] {
-    const char* e = getenv("ACEDAG_K2_SPL");
-    return e && atoi(e) == 1 ? 1 : 2;
-  }();
-  return s;
+int k2_spl_env() {
+  const char* e = getenv("ACEDAG_K2_SPL");
+  return e && atoi(e) == 1 ? 1 : 2;
 }
+int k2_mode();
+int k2_spl() { return k2_mode() == 1 ? 1 : 2; }
 
 template <int NU, typename T, int WARPS, int MAXU, bool HYB>
 cudaError_t launch_fast2_w(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
@@ -545,6 +544,67 @@ int k2_maxu() {
   }();
   return m;
 }
+
+// fp64 fast-path kernel: "tmem" (hot seeds in tensor memory), "two" (two
+// sites per lane), "one" (one site per lane); ACEDAG_K2 overrides
+int k2_mode() {
+  static int m = [] {
+    const char* e = getenv("ACEDAG_K2");
+    if (e && std::string(e) == "two") return 2;
+    if (e && std::string(e) == "one") return 1;
+    if (e && std::string(e) == "tmem") return 3;
+    if (k2_spl_env() == 1) return 1;
+    return 3;
+  }();
+  return m;
+}
+
+template <int NU, int WARPS, int MAXU, bool HYB>
+cudaError_t launch_tmem_w(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                          double* out, const Launch& lc, cudaStream_t st) {
+  auto k = dev::k2_tmem<NU, WARPS, MAXU, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  e = lc.ws->part.alloc((size_t)lc.grid * WARPS * 32);
+  if (e != cudaSuccess) return e;
+  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
+                                        out, lc.ws->gcache.p, lc.ws->part.p);
+  return cudaGetLastError();
+}
+
+template <int NU, bool HYB>
+cudaError_t launch_tmem_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                          double* out, const Launch& lc, cudaStream_t st) {
+  const int w = lc.block / 32;
+  if (w == 32) return launch_tmem_w<NU, 32, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+  if (w == 24) return launch_tmem_w<NU, 24, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+  if (k2_maxu() == 2) return launch_tmem_w<NU, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+  return launch_tmem_w<NU, 16, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
+}
+
+// geometry of k2_tmem: 32 warps, 128 hot rows in TMEM, cold rows in smem
+int tmem_launch(acedag_plan* P, int64_t S, Launch& lc) {
+  const int64_t ntiles = (S + 31) / 32;
+  const int warps = k2_warps();
+  lc.block = warps * 32;
+  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
+  lc.rows = P->U + 1;
+  const int cold = std::max(0, lc.rows - (int)dev::kTmemRows);
+  const size_t fixed = (size_t)warps * 1024 + 16;
+  const int us_max = (int)((P->smem_optin - fixed) / 512);
+  lc.us = std::min(cold, us_max);
+  lc.hyb = lc.us < cold;
+  lc.smem = (size_t)lc.us * 512 + fixed;
+  if (lc.hyb && lc.ws->gcache.alloc((size_t)lc.grid * (cold - lc.us) * 32) != cudaSuccess)
+    return fail(ACEDAG_ENOMEM, "gcache allocation failed");
+  return 0;
+}
+
+template <int NU> struct TmemF64 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_tmem_k<NU, true>(a...) : launch_tmem_k<NU, false>(a...);
+  }
+};
 
 template <int NU, typename T, bool HYB>
 cudaError_t launch_fast2(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
@@ -727,6 +787,10 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
         if (rc) return rc;
         e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
       }
+    } else if (fast && k2_mode() == 3) {
+      int rc = tmem_launch(P, S, lc);
+      if (rc) return rc;
+      e = by_order<TmemF64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
     } else if (fast) {
       if (k2_spl() == 2) {
         int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024, k2_warps(), lc, 64);

@@ -304,6 +304,205 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
   }
 }
 
+// ------------------------------------------------ K2 (TMEM-resident seeds)
+// The hot seed rows live in TENSOR MEMORY: TMEM reads (tcgen05.ld, 220 B/clk/
+// SM measured) run on a path separate from the shared-memory crossbar
+// (127 B/clk/SM), so the seed fetches no longer compete with the program
+// stream.  TMEM is 128 lanes x 512 columns x 32 bit; a warp can only reach
+// the 32 lanes of its quadrant (warp % 4), so the hot rows are replicated in
+// all four quadrants: lane i of a quadrant = site i of the 32-site tile, a
+// seed row = 4 columns (one complex128), 128 rows.  Slots >= kTmemRows (the
+// cold tail, ~6% of fetches at cfg2) stay in shared memory / the global cache.
+constexpr uint32_t kTmemRows = 128;
+
+__device__ __forceinline__ void tmem_ld4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void tmem_st4(uint32_t addr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr),
+               "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)),
+               "r"(__double2hiint(v.y)));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ double2 u4_to_c(const uint32_t (&r)[4]) {
+  return make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+}
+
+template <bool HYB>
+struct SeedsT {
+  uint32_t tq;        // TMEM address of this warp's quadrant, column 0
+  uint32_t s;         // g_smem byte offset of this lane's entry in cold row 0
+  const char* g;      // global cache (rows past the smem budget)
+  uint32_t us_rows;   // cold rows held in shared memory
+  // issue: returns true when the value will arrive through TMEM (call wait)
+  __device__ __forceinline__ bool issue(uint32_t slot, uint32_t (&t)[4], double2& v) const {
+    if (slot < kTmemRows) {
+      tmem_ld4(tq + slot * 4, t);
+      return true;
+    }
+    const uint32_t c = slot - kTmemRows;
+    if (!HYB || c < us_rows) v = *reinterpret_cast<const double2*>(g_smem + s + c * 512);
+    else v = *reinterpret_cast<const double2*>(g + (size_t)(c - us_rows) * 512);
+    return false;
+  }
+  __device__ __forceinline__ double2 get(uint32_t slot) const {
+    uint32_t t[4];
+    double2 v;
+    if (issue(slot, t, v)) {
+      tmem_wait_ld();
+      v = u4_to_c(t);
+    }
+    return v;
+  }
+};
+
+template <int K, bool HYB>
+__device__ __forceinline__ void leaf_block_t(const Stream& st, double2 pv, double& acc0, double& acc1,
+                                             const SeedsT<HYB>& sd) {
+  int4 r[K];
+  uint32_t t[K][4];
+  double2 s[K];
+  bool tm[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
+#pragma unroll
+  for (int j = 0; j < K; ++j) tm[j] = sd.issue((uint32_t)r[j].z >> 9, t[j], s[j]);
+  bool any = false;
+#pragma unroll
+  for (int j = 0; j < K; ++j) any |= tm[j];
+  if (any) tmem_wait_ld();
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (tm[j]) s[j] = u4_to_c(t[j]);
+    const double tt = s[j].x * pv.x - s[j].y * pv.y;
+    if (j & 1) acc1 += rec_c(r[j]) * tt;
+    else acc0 += rec_c(r[j]) * tt;
+  }
+}
+
+template <int MAXU, bool HYB>
+__device__ __forceinline__ void leaves_t(Stream& st, uint32_t n, double2 pv, double& acc0, double& acc1,
+                                         const SeedsT<HYB>& sd) {
+  while (n >= MAXU) {
+    leaf_block_t<MAXU, HYB>(st, pv, acc0, acc1, sd);
+    st.advance(MAXU);
+    n -= MAXU;
+  }
+  switch (n) {
+    case 1: leaf_block_t<1, HYB>(st, pv, acc0, acc1, sd); break;
+    case 2: if constexpr (MAXU > 2) leaf_block_t<2, HYB>(st, pv, acc0, acc1, sd); break;
+    case 3: if constexpr (MAXU > 3) leaf_block_t<3, HYB>(st, pv, acc0, acc1, sd); break;
+    default: break;
+  }
+  st.advance(n);
+}
+
+template <int D, int NU, int MAXU, bool HYB>
+__device__ __forceinline__ void k2t_visit(Stream& st, uint32_t n, double2 pv, double& acc0, double& acc1,
+                                          const SeedsT<HYB>& sd) {
+  if constexpr (D > NU) {
+    return;
+  } else if constexpr (D == NU) {
+    leaves_t<MAXU, HYB>(st, n, pv, acc0, acc1, sd);
+  } else {
+    for (uint32_t j = 0; j < n; ++j) {
+      const int4 r = st.at(0);
+      st.advance(1);
+      const double2 v = cmul(sd.get((uint32_t)r.z >> 9), pv);
+      acc1 += rec_c(r) * v.x;
+      k2t_visit<D + 1, NU, MAXU, HYB>(st, rec_nch(r), v, acc0, acc1, sd);
+    }
+  }
+}
+
+// Records carry slot * 512 in .z (the generic program stream).
+template <int NU, int WARPS, int MAXU, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k2_tmem(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
+        int Us_cold, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
+        double* __restrict__ out, double2* __restrict__ gcache, double* __restrict__ part) {
+  unsigned char* smem = g_smem;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rows = U + 1;                                    // U seeds + ONE
+  const int hot = rows < (int)kTmemRows ? rows : (int)kTmemRows;
+  const int cold = rows - hot;
+  const int us = cold < Us_cold ? cold : Us_cold;           // cold rows in smem
+  double2* sC = reinterpret_cast<double2*>(smem);            // [us][32]
+  const uint32_t rings = (uint32_t)((size_t)us * 512);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + rings + WARPS * 64 * 16);
+  double2* gC = HYB ? gcache + (size_t)blockIdx.x * (cold - us) * 32 : nullptr;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tbase = *tslot;
+  SeedsT<HYB> sd;
+  sd.tq = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+  sd.s = (uint32_t)(lane * 16);
+  sd.g = HYB ? reinterpret_cast<const char*>(gC) + lane * 16 : nullptr;
+  sd.us_rows = (uint32_t)us;
+  double* mypart = part + (size_t)blockIdx.x * WARPS * 32;
+  Stream st;
+  const int64_t ntiles = (S + 31) / 32;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t site = tile * 32 + lane;
+    const bool valid = site < S;
+    const double2* row = A + (valid ? site : 0) * (int64_t)L;
+    // hot rows -> TMEM, replicated per quadrant: warp w fills rows w/4, w/4 + W/4, ...
+    for (int h = warp >> 2; h < hot; h += WARPS / 4) {
+      double2 v;
+      if (h == U) v = make_double2(1.0, 0.0);
+      else v = valid ? ld_stream(row + __ldg(slot_label + h)) : make_double2(0.0, 0.0);
+      tmem_st4(sd.tq + (uint32_t)h * 4, v);
+    }
+    // cold rows -> shared memory / global cache
+    for (int c = warp; c < cold; c += WARPS) {
+      const int u = hot + c;
+      double2 v;
+      if (u == U) v = make_double2(1.0, 0.0);
+      else v = valid ? ld_stream(row + __ldg(slot_label + u)) : make_double2(0.0, 0.0);
+      if (!HYB || c < us) sC[c * 32 + lane] = v;
+      else gC[(size_t)(c - us) * 32 + lane] = v;
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    double wacc = 0.0;
+    for (int ci = warp; ci < nchunk; ci += WARPS) {
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), rings + warp * 64 * 16, lane);
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        st.advance(2);
+        double acc0 = 0, acc1 = 0;
+        const double2 v = cmul(sd.get((uint32_t)r0.z >> 9), sd.get((uint32_t)r1.z >> 9));
+        acc0 += rec_c(r0) * v.x;
+        k2t_visit<3, NU, MAXU, HYB>(st, rec_nch(r0), v, acc0, acc1, sd);
+        wacc += acc0 + acc1;
+      }
+    }
+    mypart[warp * 32 + lane] = wacc;
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (warp == 0) {
+      double s = 0.0;
+      for (int w = 0; w < WARPS; ++w) s += __ldcg(mypart + w * 32 + lane);
+      if (valid) out[site] = s;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
 // ------------------------------------------------------ K2 (two sites/lane)
 // 64-site tiles: lane handles sites t*64 + lane and t*64 + 32 + lane, so each
 // program record (and its decode) serves twice the sites.  The seed table is

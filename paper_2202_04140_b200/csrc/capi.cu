@@ -589,7 +589,7 @@ int tmem_launch(acedag_plan* P, int64_t S, Launch& lc) {
   lc.block = warps * 32;
   lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
   lc.rows = P->U + 1;
-  const int cold = std::max(0, lc.rows - (int)dev::kTmemRows);
+  const int cold = std::max(0, lc.rows - (int)kTmemRows);
   const size_t fixed = (size_t)warps * 1024 + 16;
   const int us_max = (int)((P->smem_optin - fixed) / 512);
   lc.us = std::min(cold, us_max);

@@ -313,8 +313,6 @@ k2_fast(const typename V2<T>::t* __restrict__ A, int64_t S, int L,
 // all four quadrants: lane i of a quadrant = site i of the 32-site tile, a
 // seed row = 4 columns (one complex128), 128 rows.  Slots >= kTmemRows (the
 // cold tail, ~6% of fetches at cfg2) stay in shared memory / the global cache.
-constexpr uint32_t kTmemRows = 128;
-
 __device__ __forceinline__ void tmem_ld4(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -336,83 +334,104 @@ struct SeedsT {
   uint32_t s;         // g_smem byte offset of this lane's entry in cold row 0
   const char* g;      // global cache (rows past the smem budget)
   uint32_t us_rows;   // cold rows held in shared memory
-  // issue: returns true when the value will arrive through TMEM (call wait)
-  __device__ __forceinline__ bool issue(uint32_t slot, uint32_t (&t)[4], double2& v) const {
-    if (slot < kTmemRows) {
-      tmem_ld4(tq + slot * 4, t);
-      return true;
-    }
-    const uint32_t c = slot - kTmemRows;
-    if (!HYB || c < us_rows) v = *reinterpret_cast<const double2*>(g_smem + s + c * 512);
-    else v = *reinterpret_cast<const double2*>(g + (size_t)(c - us_rows) * 512);
-    return false;
+  // records carry slot * 512; hot slots (< kTmemRows) are TMEM rows of 4 columns
+  __device__ __forceinline__ void hot_issue(uint32_t off, uint32_t (&t)[4]) const {
+    tmem_ld4(tq + (off >> 7), t);
   }
-  __device__ __forceinline__ double2 get(uint32_t slot) const {
+  __device__ __forceinline__ double2 hot(uint32_t off) const {
     uint32_t t[4];
-    double2 v;
-    if (issue(slot, t, v)) {
-      tmem_wait_ld();
-      v = u4_to_c(t);
-    }
-    return v;
+    hot_issue(off, t);
+    tmem_wait_ld();
+    return u4_to_c(t);
   }
+  __device__ __forceinline__ double2 cold(uint32_t off) const {
+    const uint32_t c = off - kTmemRows * kRowBytes;  // byte offset of the cold row
+    if (!HYB || c < us_rows * kRowBytes) return *reinterpret_cast<const double2*>(g_smem + s + c);
+    return *reinterpret_cast<const double2*>(g + (c - us_rows * kRowBytes));
+  }
+  __device__ __forceinline__ double2 get(uint32_t off, bool is_hot) const { return is_hot ? hot(off) : cold(off); }
 };
 
+// one batch of K leaves whose seeds are all TMEM-resident
 template <int K, bool HYB>
-__device__ __forceinline__ void leaf_block_t(const Stream& st, double2 pv, double& acc0, double& acc1,
-                                             const SeedsT<HYB>& sd) {
+__device__ __forceinline__ void leaf_block_hot(const Stream& st, double2 pv, double& acc0, double& acc1,
+                                               const SeedsT<HYB>& sd) {
   int4 r[K];
   uint32_t t[K][4];
-  double2 s[K];
-  bool tm[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) r[j] = st.at(j);
 #pragma unroll
-  for (int j = 0; j < K; ++j) tm[j] = sd.issue((uint32_t)r[j].z >> 9, t[j], s[j]);
-  bool any = false;
-#pragma unroll
-  for (int j = 0; j < K; ++j) any |= tm[j];
-  if (any) tmem_wait_ld();
+  for (int j = 0; j < K; ++j) sd.hot_issue((uint32_t)r[j].z, t[j]);
+  tmem_wait_ld();
 #pragma unroll
   for (int j = 0; j < K; ++j) {
-    if (tm[j]) s[j] = u4_to_c(t[j]);
-    const double tt = s[j].x * pv.x - s[j].y * pv.y;
+    const double2 sv = u4_to_c(t[j]);
+    const double tt = sv.x * pv.x - sv.y * pv.y;
     if (j & 1) acc1 += rec_c(r[j]) * tt;
     else acc0 += rec_c(r[j]) * tt;
   }
 }
 
-template <int MAXU, bool HYB>
+// one batch of K leaves whose seeds are in shared memory / the global cache
+template <int K, bool HYB>
+__device__ __forceinline__ void leaf_block_cold(const Stream& st, double2 pv, double& acc0, double& acc1,
+                                                const SeedsT<HYB>& sd) {
+  int4 r[K];
+  double2 sv[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
+#pragma unroll
+  for (int j = 0; j < K; ++j) sv[j] = sd.cold((uint32_t)r[j].z);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double tt = sv[j].x * pv.x - sv[j].y * pv.y;
+    if (j & 1) acc1 += rec_c(r[j]) * tt;
+    else acc0 += rec_c(r[j]) * tt;
+  }
+}
+
+template <bool HOT, int MAXU, bool HYB>
 __device__ __forceinline__ void leaves_t(Stream& st, uint32_t n, double2 pv, double& acc0, double& acc1,
                                          const SeedsT<HYB>& sd) {
   while (n >= MAXU) {
-    leaf_block_t<MAXU, HYB>(st, pv, acc0, acc1, sd);
+    if constexpr (HOT) leaf_block_hot<MAXU, HYB>(st, pv, acc0, acc1, sd);
+    else leaf_block_cold<MAXU, HYB>(st, pv, acc0, acc1, sd);
     st.advance(MAXU);
     n -= MAXU;
   }
-  switch (n) {
-    case 1: leaf_block_t<1, HYB>(st, pv, acc0, acc1, sd); break;
-    case 2: if constexpr (MAXU > 2) leaf_block_t<2, HYB>(st, pv, acc0, acc1, sd); break;
-    case 3: if constexpr (MAXU > 3) leaf_block_t<3, HYB>(st, pv, acc0, acc1, sd); break;
-    default: break;
+  if (n) {
+    if constexpr (MAXU > 2) {
+      if (n >= 2) {
+        if constexpr (HOT) leaf_block_hot<2, HYB>(st, pv, acc0, acc1, sd);
+        else leaf_block_cold<2, HYB>(st, pv, acc0, acc1, sd);
+        st.advance(2);
+        n -= 2;
+      }
+    }
+    if (n) {
+      if constexpr (HOT) leaf_block_hot<1, HYB>(st, pv, acc0, acc1, sd);
+      else leaf_block_cold<1, HYB>(st, pv, acc0, acc1, sd);
+      st.advance(1);
+    }
   }
-  st.advance(n);
 }
 
+// children of a node: n records, the first nh with TMEM-resident seeds
 template <int D, int NU, int MAXU, bool HYB>
-__device__ __forceinline__ void k2t_visit(Stream& st, uint32_t n, double2 pv, double& acc0, double& acc1,
-                                          const SeedsT<HYB>& sd) {
+__device__ __forceinline__ void k2t_visit(Stream& st, uint32_t n, uint32_t nh, double2 pv, double& acc0,
+                                          double& acc1, const SeedsT<HYB>& sd) {
   if constexpr (D > NU) {
     return;
   } else if constexpr (D == NU) {
-    leaves_t<MAXU, HYB>(st, n, pv, acc0, acc1, sd);
+    leaves_t<true, MAXU, HYB>(st, nh, pv, acc0, acc1, sd);
+    leaves_t<false, MAXU, HYB>(st, n - nh, pv, acc0, acc1, sd);
   } else {
     for (uint32_t j = 0; j < n; ++j) {
       const int4 r = st.at(0);
       st.advance(1);
-      const double2 v = cmul(sd.get((uint32_t)r.z >> 9), pv);
+      const double2 v = cmul(sd.get((uint32_t)r.z, j < nh), pv);
       acc1 += rec_c(r) * v.x;
-      k2t_visit<D + 1, NU, MAXU, HYB>(st, rec_nch(r), v, acc0, acc1, sd);
+      k2t_visit<D + 1, NU, MAXU, HYB>(st, rec_nch(r), (uint32_t)r.w >> 16, v, acc0, acc1, sd);
     }
   }
 }
@@ -482,9 +501,10 @@ k2_tmem(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
         const int4 r0 = st.at(0), r1 = st.at(1);
         st.advance(2);
         double acc0 = 0, acc1 = 0;
-        const double2 v = cmul(sd.get((uint32_t)r0.z >> 9), sd.get((uint32_t)r1.z >> 9));
+        const uint32_t fl = (uint32_t)r1.w >> 16;  // hot flags of the two root seeds
+        const double2 v = cmul(sd.get((uint32_t)r0.z, fl & 1u), sd.get((uint32_t)r1.z, (fl >> 1) & 1u));
         acc0 += rec_c(r0) * v.x;
-        k2t_visit<3, NU, MAXU, HYB>(st, rec_nch(r0), v, acc0, acc1, sd);
+        k2t_visit<3, NU, MAXU, HYB>(st, rec_nch(r0), (uint32_t)r0.w >> 16, v, acc0, acc1, sd);
         wacc += acc0 + acc1;
       }
     }

@@ -168,7 +168,13 @@ void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re, c
   std::vector<int32_t> roots = singles;
   roots.insert(roots.end(), by_order[2].begin(), by_order[2].end());
   std::sort(roots.begin(), roots.end(), by_tuple);
-  for (auto& n : nodes) std::sort(n.kids.begin(), n.kids.end(), by_tuple);
+  // children whose seed is TMEM-resident in k2_tmem (slot < kTmemRows) first
+  auto hot = [&](int32_t k) { return slot[nodes[k].sec] < kTmemRows; };
+  for (auto& n : nodes)
+    std::sort(n.kids.begin(), n.kids.end(), [&](int32_t a, int32_t b) {
+      if (hot(a) != hot(b)) return hot(a);
+      return nodes[a].t < nodes[b].t;
+    });
   P.max_order = std::max(2, max_order);
 
   // Records (16 B): {c, byte offset of the seed row, #children, subtree size}.
@@ -192,42 +198,43 @@ void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re, c
       if (c_im) P.cim.push_back(has ? rows_im[nodes[k].coef * n_out + o] : 0.0);
     }
   };
-  // preorder with subtree sizes patched on the way back up
-  std::vector<std::pair<int32_t, int64_t>> stack;  // (node, record index) ; node<0 = close marker
+  // preorder; `skip` = number of leading children with a TMEM-resident seed
+  // (roots: second record's skip = hot flags of the two root seeds)
+  auto nhot = [&](int32_t k) {
+    uint16_t h = 0;
+    for (int32_t q : nodes[k].kids) h += hot(q) ? 1 : 0;
+    return h;
+  };
+  std::vector<int32_t> stack;
   std::vector<int64_t> op_root;
   for (size_t r = 0; r < roots.size(); ++r) {
     int32_t k = roots[r];
     op_root.push_back((int64_t)P.ops.size());
     if (nodes[k].t.len == 1) {
-      emit(k, off_of(slot[nodes[k].t.id[0]]), 0);
+      const uint32_t s0 = slot[nodes[k].t.id[0]];
+      emit(k, off_of(s0), 0);
       emit(-1, off_of(U), 0);
+      P.ops.back().skip = (uint16_t)((s0 < kTmemRows ? 1 : 0) | (U < kTmemRows ? 2 : 0));
       root_cost[r] = 6;
       continue;
     }
-    const int64_t r0 = (int64_t)P.ops.size();
-    emit(k, off_of(slot[nodes[k].sa]), (uint32_t)nodes[k].kids.size());
-    emit(-1, off_of(slot[nodes[k].sb]), 0);
+    const uint32_t sa = slot[nodes[k].sa], sb = slot[nodes[k].sb];
+    emit(k, off_of(sa), (uint32_t)nodes[k].kids.size());
+    P.ops.back().skip = nhot(k);
+    emit(-1, off_of(sb), 0);
+    P.ops.back().skip = (uint16_t)((sa < kTmemRows ? 1 : 0) | (sb < kTmemRows ? 2 : 0));
     P.recursive_products++;
     int64_t cost = 8;
-    stack.clear();
-    for (auto it = nodes[k].kids.rbegin(); it != nodes[k].kids.rend(); ++it) stack.push_back({*it, -1});
+    stack.assign(nodes[k].kids.rbegin(), nodes[k].kids.rend());
     while (!stack.empty()) {
-      auto [q, at] = stack.back();
+      const int32_t q = stack.back();
       stack.pop_back();
-      if (at >= 0) {  // close: subtree of record `at` ends here
-        int64_t size = (int64_t)P.ops.size() - at - 1;
-        P.ops[at].skip = size <= 0xFFFE ? (uint16_t)size : (uint16_t)0xFFFF;
-        continue;
-      }
-      const int64_t me = (int64_t)P.ops.size();
       emit(q, off_of(slot[nodes[q].sec]), (uint32_t)nodes[q].kids.size());
+      P.ops.back().skip = nhot(q);
       P.recursive_products++;
       cost += nodes[q].kids.empty() ? 4 : 6;
-      stack.push_back({q, me});
-      for (auto it = nodes[q].kids.rbegin(); it != nodes[q].kids.rend(); ++it) stack.push_back({*it, -1});
+      for (auto it = nodes[q].kids.rbegin(); it != nodes[q].kids.rend(); ++it) stack.push_back(*it);
     }
-    int64_t size = (int64_t)P.ops.size() - r0 - 2;
-    P.ops[r0].skip = size <= 0xFFFE ? (uint16_t)size : (uint16_t)0xFFFF;
     root_cost[r] = cost;
   }
   // ---- work chunks at root boundaries, balanced by cost (grabbed dynamically

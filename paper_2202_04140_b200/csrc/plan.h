@@ -28,10 +28,12 @@ struct alignas(16) Op {
   double c;       // first output's real coefficient (0 if the node carries none)
   uint32_t off;   // byte offset of the seed row in the [slot][32 sites] c128 table
   uint16_t nch;   // number of children that follow in DFS preorder
-  uint16_t skip;  // records in this node's subtree (0xFFFF: too large to say)
+  uint16_t skip;  // leading children whose seed is TMEM-resident (k2_tmem);
+                  // a root's second record: bit0/bit1 = its two seeds are
 };
 constexpr uint16_t kSingle = 0xFFFF;
 constexpr uint32_t kRowBytes = 32 * 16;  // one slot row: 32 sites x complex128
+constexpr uint32_t kTmemRows = 128;        // hottest slots k2_tmem keeps in TMEM
 
 struct PlanHost {
   int max_order = 2;                 // deepest order in the recursive program

@@ -176,6 +176,10 @@ int current_device() {
 
 }  // namespace
 
+namespace {
+int k2_mode();  // fp64 fast-path kernel selection (below)
+}
+
 struct acedag_graph {
   Graph g;
 };
@@ -361,7 +365,8 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
     return fail(ACEDAG_EINVAL, "bad coefficient arguments");
   DevGuard dg(P->device);
   try {
-    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, plan_chunks(), P->host);
+    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, plan_chunks(), P->host,
+                 k2_mode() == 4 ? dev::kTmemRows2 : kTmemRows);
   } catch (const std::domain_error& e) {
     return fail(ACEDAG_ENOTTARGET, e.what());
   } catch (const std::bad_alloc&) {
@@ -553,6 +558,7 @@ int k2_mode() {
     if (e && std::string(e) == "two") return 2;
     if (e && std::string(e) == "one") return 1;
     if (e && std::string(e) == "tmem") return 3;
+    if (e && std::string(e) == "tmem2") return 4;
     if (k2_spl_env() == 1) return 1;
     return 3;
   }();
@@ -599,6 +605,50 @@ int tmem_launch(acedag_plan* P, int64_t S, Launch& lc) {
     return fail(ACEDAG_ENOMEM, "gcache allocation failed");
   return 0;
 }
+
+template <int NU, int WARPS, int MAXU, bool HYB>
+cudaError_t launch_tmem2_w(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                           double* out, const Launch& lc, cudaStream_t st) {
+  auto k = dev::k2_tmem2<NU, WARPS, MAXU, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  e = lc.ws->part.alloc((size_t)lc.grid * WARPS * 64);
+  if (e != cudaSuccess) return e;
+  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
+                                        out, lc.ws->gcache.p, lc.ws->part.p);
+  return cudaGetLastError();
+}
+
+template <int NU, bool HYB>
+cudaError_t launch_tmem2_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                           double* out, const Launch& lc, cudaStream_t st) {
+  if (lc.block == 32 * 32) return launch_tmem2_w<NU, 32, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+  return launch_tmem2_w<NU, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+}
+
+// geometry of k2_tmem2: 64-site tiles, 64 hot rows in TMEM, 1 KB cold rows
+int tmem2_launch(acedag_plan* P, int64_t S, Launch& lc) {
+  const int64_t ntiles = (S + 63) / 64;
+  const int warps = k2_warps() == 16 ? 16 : 32;
+  lc.block = warps * 32;
+  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
+  lc.rows = P->U + 1;
+  const int cold = std::max(0, lc.rows - (int)dev::kTmemRows2);
+  const size_t fixed = (size_t)warps * 1024 + 16;
+  const int us_max = (int)((P->smem_optin - fixed) / 1024);
+  lc.us = std::min(cold, us_max);
+  lc.hyb = lc.us < cold;
+  lc.smem = (size_t)lc.us * 1024 + fixed;
+  if (lc.hyb && lc.ws->gcache.alloc((size_t)lc.grid * (cold - lc.us) * 64) != cudaSuccess)
+    return fail(ACEDAG_ENOMEM, "gcache allocation failed");
+  return 0;
+}
+
+template <int NU> struct Tmem2F64 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_tmem2_k<NU, true>(a...) : launch_tmem2_k<NU, false>(a...);
+  }
+};
 
 template <int NU> struct TmemF64 {
   template <typename... A> static cudaError_t run(bool hyb, A... a) {
@@ -787,6 +837,10 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
         if (rc) return rc;
         e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
       }
+    } else if (fast && k2_mode() == 4) {
+      int rc = tmem2_launch(P, S, lc);
+      if (rc) return rc;
+      e = by_order<Tmem2F64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
     } else if (fast && k2_mode() == 3) {
       int rc = tmem_launch(P, S, lc);
       if (rc) return rc;

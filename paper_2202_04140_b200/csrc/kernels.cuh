@@ -523,6 +523,235 @@ k2_tmem(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
 }
 
+// --------------------------------------- K2 (TMEM seeds, two sites per lane)
+// 64-site tiles: lane holds sites t*64 + lane and t*64 + 32 + lane.  A hot
+// TMEM row (64 rows, replicated per quadrant) is 8 columns = the seed of both
+// sites, so ONE tcgen05.ld.32x32b.x8 serves two products.  Slots >= 64 come
+// from shared memory rows [64 sites] (1 KB) or the global cache.
+constexpr uint32_t kTmemRows2 = 64;
+
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t addr, double2 a, double2 b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(addr),
+               "r"(__double2loint(a.x)), "r"(__double2hiint(a.x)), "r"(__double2loint(a.y)), "r"(__double2hiint(a.y)),
+               "r"(__double2loint(b.x)), "r"(__double2hiint(b.x)), "r"(__double2loint(b.y)), "r"(__double2hiint(b.y)));
+}
+
+template <bool HYB>
+struct SeedsT2 {
+  uint32_t tq;        // TMEM address of this warp's quadrant, column 0
+  uint32_t s;         // g_smem byte offset of this lane's entry (site A) in cold row 0
+  const char* g;      // global cache base + lane * 16
+  uint32_t us_rows;   // cold rows in shared memory
+  __device__ __forceinline__ void hot_issue(uint32_t off, uint32_t (&t)[8]) const { tmem_ld8(tq + (off >> 6), t); }
+  __device__ __forceinline__ void cold(uint32_t off, double2& a, double2& b) const {
+    const uint32_t c = (off - kTmemRows2 * kRowBytes) * 2;  // byte offset of the 1 KB cold row
+    if (!HYB || c < us_rows * 1024u) {
+      a = *reinterpret_cast<const double2*>(g_smem + s + c);
+      b = *reinterpret_cast<const double2*>(g_smem + s + c + 512);
+    } else {
+      a = *reinterpret_cast<const double2*>(g + (c - us_rows * 1024u));
+      b = *reinterpret_cast<const double2*>(g + (c - us_rows * 1024u) + 512);
+    }
+  }
+  __device__ __forceinline__ void get(uint32_t off, bool hot, double2& a, double2& b) const {
+    if (hot) {
+      uint32_t t[8];
+      hot_issue(off, t);
+      tmem_wait_ld();
+      a = make_double2(__hiloint2double(t[1], t[0]), __hiloint2double(t[3], t[2]));
+      b = make_double2(__hiloint2double(t[5], t[4]), __hiloint2double(t[7], t[6]));
+    } else {
+      cold(off, a, b);
+    }
+  }
+};
+
+template <bool HOT, int K, bool HYB>
+__device__ __forceinline__ void leaf_block_t2(const Stream& st, double2 pa, double2 pb, double& acc0, double& acc1,
+                                              const SeedsT2<HYB>& sd) {
+  int4 r[K];
+  double2 sa[K], sb[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
+  if constexpr (HOT) {
+    uint32_t t[K][8];
+#pragma unroll
+    for (int j = 0; j < K; ++j) sd.hot_issue((uint32_t)r[j].z, t[j]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      sa[j] = make_double2(__hiloint2double(t[j][1], t[j][0]), __hiloint2double(t[j][3], t[j][2]));
+      sb[j] = make_double2(__hiloint2double(t[j][5], t[j][4]), __hiloint2double(t[j][7], t[j][6]));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) sd.cold((uint32_t)r[j].z, sa[j], sb[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double c = rec_c(r[j]);
+    acc0 += c * (sa[j].x * pa.x - sa[j].y * pa.y);
+    acc1 += c * (sb[j].x * pb.x - sb[j].y * pb.y);
+  }
+}
+
+template <bool HOT, int MAXU, bool HYB>
+__device__ __forceinline__ void leaves_t2(Stream& st, uint32_t n, double2 pa, double2 pb, double& acc0,
+                                          double& acc1, const SeedsT2<HYB>& sd) {
+  while (n >= MAXU) {
+    leaf_block_t2<HOT, MAXU, HYB>(st, pa, pb, acc0, acc1, sd);
+    st.advance(MAXU);
+    n -= MAXU;
+  }
+  if constexpr (MAXU > 2) {
+    if (n >= 2) {
+      leaf_block_t2<HOT, 2, HYB>(st, pa, pb, acc0, acc1, sd);
+      st.advance(2);
+      n -= 2;
+    }
+  }
+  if (n) {
+    leaf_block_t2<HOT, 1, HYB>(st, pa, pb, acc0, acc1, sd);
+    st.advance(1);
+  }
+}
+
+template <int D, int NU, int MAXU, bool HYB>
+__device__ __forceinline__ void k2t2_visit(Stream& st, uint32_t n, uint32_t nh, double2 pa, double2 pb,
+                                           double& acc0, double& acc1, const SeedsT2<HYB>& sd) {
+  if constexpr (D > NU) {
+    return;
+  } else if constexpr (D == NU) {
+    leaves_t2<true, MAXU, HYB>(st, nh, pa, pb, acc0, acc1, sd);
+    leaves_t2<false, MAXU, HYB>(st, n - nh, pa, pb, acc0, acc1, sd);
+  } else {
+    for (uint32_t j = 0; j < n; ++j) {
+      const int4 r = st.at(0);
+      st.advance(1);
+      double2 sa, sb;
+      sd.get((uint32_t)r.z, j < nh, sa, sb);
+      const double2 va = cmul(sa, pa), vb = cmul(sb, pb);
+      const double c = rec_c(r);
+      acc0 += c * va.x;
+      acc1 += c * vb.x;
+      k2t2_visit<D + 1, NU, MAXU, HYB>(st, rec_nch(r), (uint32_t)r.w >> 16, va, vb, acc0, acc1, sd);
+    }
+  }
+}
+
+template <int NU, int WARPS, int MAXU, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k2_tmem2(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
+         int Us_cold, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
+         double* __restrict__ out, double2* __restrict__ gcache, double* __restrict__ part) {
+  unsigned char* smem = g_smem;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rows = U + 1;
+  const int hot = rows < (int)kTmemRows2 ? rows : (int)kTmemRows2;
+  const int cold = rows - hot;
+  const int us = cold < Us_cold ? cold : Us_cold;
+  double2* sC = reinterpret_cast<double2*>(smem);            // [us][64]
+  const uint32_t rings = (uint32_t)((size_t)us * 1024);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + rings + WARPS * 64 * 16);
+  double2* gC = HYB ? gcache + (size_t)blockIdx.x * (cold - us) * 64 : nullptr;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tbase = *tslot;
+  SeedsT2<HYB> sd;
+  sd.tq = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+  sd.s = (uint32_t)(lane * 16);
+  sd.g = HYB ? reinterpret_cast<const char*>(gC) + lane * 16 : nullptr;
+  sd.us_rows = (uint32_t)us;
+  double* mypart = part + (size_t)blockIdx.x * WARPS * 64;
+  Stream st;
+  const int64_t ntiles = (S + 63) / 64;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t sa_i = tile * 64 + lane, sb_i = sa_i + 32;
+    const bool va_ok = sa_i < S, vb_ok = sb_i < S;
+    const double2* rowa = A + (va_ok ? sa_i : 0) * (int64_t)L;
+    const double2* rowb = A + (vb_ok ? sb_i : 0) * (int64_t)L;
+    for (int h = warp >> 2; h < hot; h += WARPS / 4) {
+      double2 a, b;
+      if (h == U) {
+        a = b = make_double2(1.0, 0.0);
+      } else {
+        const int lab = __ldg(slot_label + h);
+        a = va_ok ? ld_stream(rowa + lab) : make_double2(0.0, 0.0);
+        b = vb_ok ? ld_stream(rowb + lab) : make_double2(0.0, 0.0);
+      }
+      tmem_st8(sd.tq + (uint32_t)h * 8, a, b);
+    }
+    for (int c = warp; c < cold; c += WARPS) {
+      const int u = hot + c;
+      double2 a, b;
+      if (u == U) {
+        a = b = make_double2(1.0, 0.0);
+      } else {
+        const int lab = __ldg(slot_label + u);
+        a = va_ok ? ld_stream(rowa + lab) : make_double2(0.0, 0.0);
+        b = vb_ok ? ld_stream(rowb + lab) : make_double2(0.0, 0.0);
+      }
+      if (!HYB || c < us) {
+        sC[c * 64 + lane] = a;
+        sC[c * 64 + 32 + lane] = b;
+      } else {
+        gC[(size_t)(c - us) * 64 + lane] = a;
+        gC[(size_t)(c - us) * 64 + 32 + lane] = b;
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    double wa = 0.0, wb = 0.0;
+    for (int ci = warp; ci < nchunk; ci += WARPS) {
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), rings + warp * 64 * 16, lane);
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        st.advance(2);
+        double acc0 = 0, acc1 = 0;
+        const uint32_t fl = (uint32_t)r1.w >> 16;
+        double2 a0, b0, a1, b1;
+        sd.get((uint32_t)r0.z, fl & 1u, a0, b0);
+        sd.get((uint32_t)r1.z, (fl >> 1) & 1u, a1, b1);
+        const double2 va = cmul(a0, a1), vb = cmul(b0, b1);
+        const double c = rec_c(r0);
+        acc0 += c * va.x;
+        acc1 += c * vb.x;
+        k2t2_visit<3, NU, MAXU, HYB>(st, rec_nch(r0), (uint32_t)r0.w >> 16, va, vb, acc0, acc1, sd);
+        wa += acc0;
+        wb += acc1;
+      }
+    }
+    mypart[(warp * 2 + 0) * 32 + lane] = wa;
+    mypart[(warp * 2 + 1) * 32 + lane] = wb;
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (warp < 2) {
+      double s = 0.0;
+      for (int w = 0; w < WARPS; ++w) s += __ldcg(mypart + (w * 2 + warp) * 32 + lane);
+      const int64_t site = tile * 64 + warp * 32 + lane;
+      if (site < S) out[site] = s;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
 // ------------------------------------------------------ K2 (two sites/lane)
 // 64-site tiles: lane handles sites t*64 + lane and t*64 + 32 + lane, so each
 // program record (and its decode) serves twice the sites.  The seed table is

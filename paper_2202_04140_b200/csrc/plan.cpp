@@ -34,7 +34,7 @@ Tuple drop_at(const Tuple& t, int pos) {
 }  // namespace
 
 void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re, const double* c_im,
-                  int64_t n_coef, int n_out, int warps, PlanHost& P) {
+                  int64_t n_coef, int n_out, int warps, PlanHost& P, uint32_t hot_rows) {
   const int64_t N = (int64_t)g.tuples.size();
   const int64_t L = g.n_seeds();
   if (n_out < 1) throw std::invalid_argument("n_out must be >= 1");
@@ -168,8 +168,8 @@ void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re, c
   std::vector<int32_t> roots = singles;
   roots.insert(roots.end(), by_order[2].begin(), by_order[2].end());
   std::sort(roots.begin(), roots.end(), by_tuple);
-  // children whose seed is TMEM-resident in k2_tmem (slot < kTmemRows) first
-  auto hot = [&](int32_t k) { return slot[nodes[k].sec] < kTmemRows; };
+  // children whose seed is TMEM-resident (slot < hot_rows) first
+  auto hot = [&](int32_t k) { return slot[nodes[k].sec] < hot_rows; };
   for (auto& n : nodes)
     std::sort(n.kids.begin(), n.kids.end(), [&](int32_t a, int32_t b) {
       if (hot(a) != hot(b)) return hot(a);
@@ -214,7 +214,7 @@ void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re, c
       const uint32_t s0 = slot[nodes[k].t.id[0]];
       emit(k, off_of(s0), 0);
       emit(-1, off_of(U), 0);
-      P.ops.back().skip = (uint16_t)((s0 < kTmemRows ? 1 : 0) | (U < kTmemRows ? 2 : 0));
+      P.ops.back().skip = (uint16_t)((s0 < hot_rows ? 1 : 0) | (U < hot_rows ? 2 : 0));
       root_cost[r] = 6;
       continue;
     }
@@ -222,7 +222,7 @@ void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re, c
     emit(k, off_of(sa), (uint32_t)nodes[k].kids.size());
     P.ops.back().skip = nhot(k);
     emit(-1, off_of(sb), 0);
-    P.ops.back().skip = (uint16_t)((sa < kTmemRows ? 1 : 0) | (sb < kTmemRows ? 2 : 0));
+    P.ops.back().skip = (uint16_t)((sa < hot_rows ? 1 : 0) | (sb < hot_rows ? 2 : 0));
     P.recursive_products++;
     int64_t cost = 8;
     stack.assign(nodes[k].kids.rbegin(), nodes[k].kids.rend());

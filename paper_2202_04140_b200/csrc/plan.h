@@ -55,8 +55,11 @@ struct PlanHost {
 
 // Throws std::invalid_argument (bad node id) or std::domain_error (non-target;
 // message carries the tuple repr).
+// hot_rows: seed slots below it are TMEM-resident in the k2_tmem kernels;
+// each node's children are ordered with those first and counted in `skip`
 void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re,
-                  const double* c_im, int64_t n_coef, int n_out, int warps, PlanHost& out);
+                  const double* c_im, int64_t n_coef, int n_out, int warps, PlanHost& out,
+                  uint32_t hot_rows = kTmemRows);
 
 std::string node_repr(const Graph& g, int64_t node);
 

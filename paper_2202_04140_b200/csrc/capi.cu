@@ -550,8 +550,9 @@ int k2_maxu() {
   return m;
 }
 
-// fp64 fast-path kernel: "tmem" (hot seeds in tensor memory), "two" (two
-// sites per lane), "one" (one site per lane); ACEDAG_K2 overrides
+// fp64 fast-path kernel: "tmem2" (default: two sites per lane, hot seeds in
+// tensor memory), "tmem" (one site per lane, hot seeds in TMEM), "two" (two
+// sites per lane, shared memory only), "one"; ACEDAG_K2 overrides
 int k2_mode() {
   static int m = [] {
     const char* e = getenv("ACEDAG_K2");
@@ -560,7 +561,7 @@ int k2_mode() {
     if (e && std::string(e) == "tmem") return 3;
     if (e && std::string(e) == "tmem2") return 4;
     if (k2_spl_env() == 1) return 1;
-    return 3;
+    return 4;  // measured fastest at cfg2 (profiles/r01)
   }();
   return m;
 }
@@ -622,14 +623,18 @@ cudaError_t launch_tmem2_w(acedag_plan* P, const double2* A, int64_t S, int L, c
 template <int NU, bool HYB>
 cudaError_t launch_tmem2_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
                            double* out, const Launch& lc, cudaStream_t st) {
-  if (lc.block == 32 * 32) return launch_tmem2_w<NU, 32, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+  if (lc.block == 32 * 32) {
+    if (k2_maxu() == 4) return launch_tmem2_w<NU, 32, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
+    return launch_tmem2_w<NU, 32, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
+  }
+  if (lc.block == 24 * 32) return launch_tmem2_w<NU, 24, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
   return launch_tmem2_w<NU, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
 }
 
 // geometry of k2_tmem2: 64-site tiles, 64 hot rows in TMEM, 1 KB cold rows
 int tmem2_launch(acedag_plan* P, int64_t S, Launch& lc) {
   const int64_t ntiles = (S + 63) / 64;
-  const int warps = k2_warps() == 16 ? 16 : 32;
+  const int warps = k2_warps();
   lc.block = warps * 32;
   lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
   lc.rows = P->U + 1;

@@ -910,6 +910,28 @@ int acedag_eval(const acedag_plan* Pc, int method, int prec, int out_kind, const
                    (cudaStream_t)stream);
 }
 
+const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, int out_kind) {
+  if (!P || !P->has_coef) {
+    fail(ACEDAG_EINVAL, "plan has no coefficients");
+    return "";
+  }
+  const PlanHost& H = P->host;
+  const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
+  if (method == ACEDAG_METHOD_NAIVE) return "k3_naive";
+  if (prec == ACEDAG_PREC_F32) return k2_spl() == 2 ? "k2_fast2 (fp32)" : "k2_fast (fp32)";
+  if (fast) {
+    switch (k2_mode()) {
+      case 4: return "k2_tmem2";
+      case 3: return "k2_tmem";
+      case 2: return "k2_fast2";
+      default: return "k2_fast";
+    }
+  }
+  if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out >= 8 && use_mma()) return "k2_mma";
+  if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out % 2 == 0) return "k2_multi";
+  return "k2_general";
+}
+
 int acedag_reduce_sites(const acedag_plan* P, const double* phi, int64_t S, double* out_total,
                         void* stream) {
   if (!P || !out_total || (S > 0 && !phi)) return fail(ACEDAG_EINVAL, "NULL argument");

@@ -162,6 +162,13 @@ class SitePlan:
         self.complex_coef = cplx
         return self
 
+    def kernel_name(self, method: str = "recursive", prec: str = "f64", out: str = "real") -> str:
+        """The kernel evaluate() launches for these arguments (reporting)."""
+        return N.lib().acedag_eval_kernel_name(
+            self._h, N.METHOD_NAIVE if method == "naive" else N.METHOD_RECURSIVE,
+            N.PREC_F32 if prec == "f32" else N.PREC_F64, N.OUT_COMPLEX if out == "complex" else N.OUT_REAL
+        ).decode()
+
     def info(self) -> dict:
         a, b, c, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
         N.check(N.lib().acedag_plan_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))

@@ -427,10 +427,12 @@ def run_ours(a):
         torch.cuda.synchronize()
         ems = max_over_ranks(e0.elapsed_time(e1) / k)
         e2e = {"value": global_sites / (ems * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size()),
+               "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size()) if pos else int(plan.last_h2d_bytes),
                "d2h_bytes_per_step": int(res.numel() * 8), "ms_per_step": ems,
-               "path": "SitePlan.evaluate%s_host: pinned host input -> 2-stream chunked H2D / kernels / D2H"
-                       % ("_positions" if pos else "")}
+               "path": ("SitePlan.evaluate_positions_host: pinned host xyz -> 2-stream chunked H2D / "
+                        "pool + K2 / D2H") if pos else
+                       ("SitePlan.evaluate_host -> acedag_eval_host: pinned host A read in place over PCIe, "
+                        "used seed columns only (k_gather_seeds on 4 SMs) pipelined with K2 on the rest, D2H")}
         del Xh
 
     F = census["F_site"]

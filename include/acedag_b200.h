@@ -149,6 +149,18 @@ const char* acedag_eval_kernel_name(const acedag_plan* plan, int method, int pre
 int acedag_eval(const acedag_plan* plan, int method, int prec, int out_kind,
                 const void* A, int64_t S, void* out, void* stream);
 
+/* acedag_eval on HOST buffers, end to end (evaluate_model's host-side call,
+ * evaluator.py:124-142, for S sites at once).  A_host: c128 (F64) / c64 (F32)
+ * [S, L]; out_host: as acedag_eval's out.  Page-locked A_host is read in
+ * place over PCIe by a gather kernel that fetches only the seed columns the
+ * plan uses, pipelined with the evaluation kernels; pageable A_host is copied
+ * in row chunks.  Ordered after prior work on `stream`; synchronous (returns
+ * with out_host written).  *h2d_bytes (may be NULL) receives the input bytes
+ * moved host->device. */
+int acedag_eval_host(const acedag_plan* plan, int method, int prec, int out_kind,
+                     const void* A_host, int64_t S, void* out_host, int64_t* h2d_bytes,
+                     void* stream);
+
 /* Batched naive_eval (evaluator.py:113-121): out[r] = prod_t vals[r, t],
  * left to right from 1+0j with separate roundings (bit-identical).  vals:
  * device c128 [n_rows, width]; lens: device int32 [n_rows] (NULL = width). */

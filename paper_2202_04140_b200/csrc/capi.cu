@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -195,6 +196,10 @@ struct acedag_plan {
   int U = 0;
   DevBuf<uint16_t> slot_label, slot_identity;
   DevBuf<int32_t> used_labels;
+  // host-path compact layout: used labels ascending (coalesced gather) and
+  // each slot's column in it
+  DevBuf<int32_t> sorted_labels;
+  DevBuf<uint16_t> slot_sorted;
   DevBuf<int32_t> col_of;  // label -> seed slot or -1 (pool of used labels only)
   DevBuf<int4> tri;        // (n, l, m >= 0) triples the used labels need
   DevBuf<Op> ops;
@@ -212,6 +217,29 @@ struct acedag_plan {
   };
   std::mutex ws_mu;
   std::map<void*, std::unique_ptr<Workspace>> wss;
+  // acedag_eval_host pipeline: gather/copy stream, evaluation stream, double
+  // buffered device chunks of seeds and results
+  struct HostPipe {
+    cudaStream_t sg = nullptr, sk = nullptr;
+    cudaEvent_t start = nullptr, gdone[2] = {}, kdone[2] = {};
+    DevBuf<unsigned char> buf[2], out[2];
+    ~HostPipe() {
+      if (sg) cudaStreamDestroy(sg);
+      if (sk) cudaStreamDestroy(sk);
+      for (cudaEvent_t e : {start, gdone[0], gdone[1], kdone[0], kdone[1]})
+        if (e) cudaEventDestroy(e);
+    }
+    cudaError_t init() {
+      if (sg) return cudaSuccess;
+      cudaError_t e = cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking);
+      for (cudaEvent_t* ev : {&start, &gdone[0], &gdone[1], &kdone[0], &kdone[1]})
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+      return e;
+    }
+  };
+  std::mutex host_mu;
+  HostPipe pipe;
   Workspace* ws(cudaStream_t s) {
     std::lock_guard<std::mutex> lk(ws_mu);
     auto& w = wss[(void*)s];
@@ -384,6 +412,15 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   CK(P->slot_identity.upload(ident));
   CK(P->used_labels.upload(used));
   {
+    std::vector<int32_t> sorted(used);
+    std::sort(sorted.begin(), sorted.end());
+    std::vector<uint16_t> pos(P->U);
+    for (int i = 0; i < P->U; ++i)
+      pos[i] = (uint16_t)(std::lower_bound(sorted.begin(), sorted.end(), used[i]) - sorted.begin());
+    CK(P->sorted_labels.upload(sorted));
+    CK(P->slot_sorted.upload(pos));
+  }
+  {
     std::vector<int32_t> col((size_t)P->g->n_seeds(), -1);
     for (int i = 0; i < P->U; ++i) col[H.slot_label[i]] = i;
     CK(P->col_of.upload(col));
@@ -458,6 +495,22 @@ namespace {
 constexpr int kWarps = 32;  // general / naive kernels
 constexpr int kNC = 8;
 
+// SMs a concurrent kernel of the same call keeps (the host-path seed gather
+// runs next to the persistent K2 grid); per thread so calls stay independent
+thread_local int t_sm_reserve = 0;
+// CTAs of the host-path seed gather (ACEDAG_GATHER_CTAS overrides)
+int gather_ctas() {
+  static int v = [] {
+    const char* e = getenv("ACEDAG_GATHER_CTAS");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  return v;
+}
+bool host_trace() {
+  static bool v = getenv("ACEDAG_HOST_TRACE") != nullptr;
+  return v;
+}
+
 struct Launch {
   int grid, block, us, rows;
   size_t smem;
@@ -482,7 +535,7 @@ int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, int wa
                 int tile = 32) {
   const int64_t ntiles = (S + tile - 1) / tile;
   lc.block = warps * 32;
-  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
+  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
   lc.rows = P->U + 1;
   size_t avail = P->smem_optin > red_bytes ? P->smem_optin - red_bytes : 0;
   int us_max = (int)(avail / (tile * elem));
@@ -594,7 +647,7 @@ int tmem_launch(acedag_plan* P, int64_t S, Launch& lc) {
   const int64_t ntiles = (S + 31) / 32;
   const int warps = k2_warps();
   lc.block = warps * 32;
-  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
+  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
   lc.rows = P->U + 1;
   const int cold = std::max(0, lc.rows - (int)kTmemRows);
   const size_t fixed = (size_t)warps * 1024 + 16;
@@ -638,7 +691,7 @@ int tmem2_launch(acedag_plan* P, int64_t S, Launch& lc) {
   const int64_t ntiles = (S + 63) / 64;
   const int warps = k2_warps();
   lc.block = warps * 32;
-  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms));
+  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
   lc.rows = P->U + 1;
   const int cold = std::max(0, lc.rows - (int)dev::kTmemRows2);
   const size_t fixed = (size_t)warps * 1024 + 16;
@@ -910,6 +963,105 @@ int acedag_eval(const acedag_plan* Pc, int method, int prec, int out_kind, const
   DevGuard dg(P->device);
   return eval_impl(P, method, prec, out_kind, A, S, (int)P->g->n_seeds(), P->slot_label.p, out,
                    (cudaStream_t)stream);
+}
+
+int acedag_eval_host(const acedag_plan* Pc, int method, int prec, int out_kind, const void* A_host, int64_t S,
+                     void* out_host, int64_t* h2d_bytes, void* stream) {
+  acedag_plan* P = const_cast<acedag_plan*>(Pc);
+  if (!P || ((!out_host || !A_host) && S > 0)) return fail(ACEDAG_EINVAL, "NULL argument");
+  if (!P->has_coef) return fail(ACEDAG_EINVAL, "plan has no coefficients (acedag_plan_set_coefficients)");
+  if (method != ACEDAG_METHOD_RECURSIVE && method != ACEDAG_METHOD_NAIVE)
+    return fail(ACEDAG_EINVAL, "unknown method");
+  if (prec != ACEDAG_PREC_F64 && prec != ACEDAG_PREC_F32) return fail(ACEDAG_EINVAL, "unknown precision");
+  if (out_kind != ACEDAG_OUT_REAL && out_kind != ACEDAG_OUT_COMPLEX)
+    return fail(ACEDAG_EINVAL, "unknown output kind");
+  if (S < 0) return fail(ACEDAG_EINVAL, "negative site count");
+  if (h2d_bytes) *h2d_bytes = 0;
+  if (S == 0) return ACEDAG_OK;
+  DevGuard dg(P->device);
+  std::lock_guard<std::mutex> lk(P->host_mu);
+  acedag_plan::HostPipe& H = P->pipe;
+  cudaError_t e = H.init();
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline streams");
+  const size_t esz = prec == ACEDAG_PREC_F32 ? 8 : 16;
+  const size_t ow = (size_t)P->host.n_out * (out_kind == ACEDAG_OUT_COMPLEX ? 16 : 8);
+  const int L = (int)P->g->n_seeds(), U = P->U;
+  // page-locked input is device-mapped (unified addressing): gather in place
+  cudaPointerAttributes at;
+  const bool mapped = cudaPointerGetAttributes(&at, A_host) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+                      at.devicePointer != nullptr;
+  cudaGetLastError();
+  const int width = mapped ? U : L;
+  // two K2 rounds of 64-site tiles per chunk on the SMs the gather leaves free
+  const int64_t chunk = std::min<int64_t>(S, (int64_t)2 * 64 * (P->sms - gather_ctas()));
+  for (int b = 0; b < 2; ++b) {
+    if (H.buf[b].alloc((size_t)chunk * width * esz) != cudaSuccess || H.out[b].alloc((size_t)chunk * ow) != cudaSuccess)
+      return fail(ACEDAG_ENOMEM, "host pipeline buffers");
+  }
+  if ((e = cudaEventRecord(H.start, (cudaStream_t)stream)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(H.sg, H.start, 0)) != cudaSuccess || (e = cudaStreamWaitEvent(H.sk, H.start, 0)) != cudaSuccess)
+    return cuda_fail(e, "host pipeline ordering");
+  const char* src = static_cast<const char*>(mapped ? at.devicePointer : A_host);
+  char* dst = static_cast<char*>(out_host);
+  int rc = ACEDAG_OK;
+  t_sm_reserve = mapped ? gather_ctas() : 0;
+  std::vector<cudaEvent_t> tr;  // ACEDAG_HOST_TRACE: per-chunk stage timings
+  auto mark = [&](cudaStream_t s) {
+    if (!host_trace()) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, s);
+    tr.push_back(ev);
+  };
+  mark(H.sg);
+  for (int64_t s0 = 0, i = 0; s0 < S && rc == ACEDAG_OK; s0 += chunk, ++i) {
+    const int b = (int)(i & 1);
+    const int64_t n = std::min(chunk, S - s0);
+    if (i >= 2) cudaStreamWaitEvent(H.sg, H.kdone[b], 0);  // K2 of chunk i-2 is done with buf[b]
+    mark(H.sg);
+    if (mapped) {
+      if (esz == 16)
+        dev::k_gather_seeds<double2><<<gather_ctas(), 512, U * 4, H.sg>>>(
+            reinterpret_cast<const double2*>(src) + s0 * L, n, L, P->sorted_labels.p, U,
+            reinterpret_cast<double2*>(H.buf[b].p));
+      else
+        dev::k_gather_seeds<float2><<<gather_ctas(), 512, U * 4, H.sg>>>(
+            reinterpret_cast<const float2*>(src) + s0 * L, n, L, P->sorted_labels.p, U,
+            reinterpret_cast<float2*>(H.buf[b].p));
+      e = cudaGetLastError();
+    } else {
+      e = cudaMemcpyAsync(H.buf[b].p, src + (size_t)s0 * L * esz, (size_t)n * L * esz, cudaMemcpyHostToDevice, H.sg);
+    }
+    if (e != cudaSuccess) { rc = cuda_fail(e, "host pipeline input"); break; }
+    mark(H.sg);
+    cudaEventRecord(H.gdone[b], H.sg);
+    cudaStreamWaitEvent(H.sk, H.gdone[b], 0);
+    mark(H.sk);
+    rc = eval_impl(P, method, prec, out_kind, H.buf[b].p, n, width, mapped ? P->slot_sorted.p : P->slot_label.p,
+                   H.out[b].p, H.sk);
+    if (rc) break;
+    mark(H.sk);
+    cudaEventRecord(H.kdone[b], H.sk);
+    e = cudaMemcpyAsync(dst + (size_t)s0 * ow, H.out[b].p, (size_t)n * ow, cudaMemcpyDeviceToHost, H.sk);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline output");
+  }
+  t_sm_reserve = 0;
+  mark(H.sk);
+  cudaError_t e1 = cudaStreamSynchronize(H.sg), e2 = cudaStreamSynchronize(H.sk);
+  if (!tr.empty()) {
+    // [start, (gather begin, gather end, eval begin, eval end) per chunk..., end]
+    for (size_t k = 1; k < tr.size(); ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tr[0], tr[k]);
+      fprintf(stderr, "%s%.3f", k == 1 ? "host trace ms:" : (k % 4 == 1 ? " |" : " "), ms);
+    }
+    fprintf(stderr, "\n");
+    for (cudaEvent_t ev : tr) cudaEventDestroy(ev);
+  }
+  if (rc) return rc;
+  if (e1 != cudaSuccess || e2 != cudaSuccess) return cuda_fail(e1 != cudaSuccess ? e1 : e2, "host pipeline");
+  if (h2d_bytes) *h2d_bytes = S * (int64_t)width * (int64_t)esz;
+  return ACEDAG_OK;
 }
 
 const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, int out_kind) {

@@ -1186,6 +1186,39 @@ k2_mma(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restri
   }
 }
 
+// ----------------------------------------------- seed gather from host rows
+// The host end-to-end path: one warp per site row reads the used seed columns
+// of the (page-locked, device-mapped) host table over PCIe -- consecutive
+// lanes read consecutive used columns, so the runs of used labels coalesce --
+// and writes the compact [S, U] table the K2 kernels then read with the
+// identity slot map.  Launched on a few SMs next to the evaluation kernel.
+template <typename T>
+__global__ void __launch_bounds__(512) k_gather_seeds(const T* __restrict__ A, int64_t S, int L,
+                                                      const int32_t* __restrict__ cols, int U, T* __restrict__ out) {
+  extern __shared__ int32_t g_cols[];
+  for (int i = threadIdx.x; i < U; i += blockDim.x) g_cols[i] = cols[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < S; s += nw) {
+    const T* row = A + s * L;
+    T* dst = out + s * U;
+    for (int j0 = 0; j0 < U; j0 += 32 * 8) {
+      T v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = j0 + lane + 32 * k;
+        if (j < U) v[k] = __ldcs(row + g_cols[j]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = j0 + lane + 32 * k;
+        if (j < U) dst[j] = v[k];
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- K2 (general)
 // complex coefficients and/or complex output and/or several outputs: NC
 // complex accumulators per lane; coefficient table [n_records, n_out].

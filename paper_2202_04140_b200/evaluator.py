@@ -202,16 +202,40 @@ class SitePlan:
         N.check(N.lib().acedag_eval(self._h, m, prec, kind, _vp(A), S, _vp(result), _stream(A.device)))
         return result
 
-    def evaluate_host(self, A: torch.Tensor, method: str = "recursive", chunk: int = 16384,
-                      result: torch.Tensor | None = None, sync: bool = True) -> torch.Tensor:
-        """End-to-end call on HOST buffers: A is a (pinned) CPU complex tensor
-        [S, L]; chunks are copied to the device, evaluated and copied back on
-        two streams so the PCIe transfers overlap the kernels.  Returns a
-        pinned float64 [S] (real output, one coefficient vector)."""
+    def evaluate_host(self, A: torch.Tensor, method: str = "recursive", out: str = "real",
+                      result: torch.Tensor | None = None) -> torch.Tensor:
+        """End-to-end call on HOST buffers (acedag_eval_host): A is a CPU
+        complex128 (or complex64, fp32 recursive mode) tensor [S, L].  Pinned
+        A is read in place by the GPU -- only the seed columns the plan uses
+        -- pipelined with the kernels; pageable A is copied in row chunks.
+        Returns a CPU tensor (pinned unless ``result`` is given) shaped like
+        :meth:`evaluate`'s; synchronous.  ``self.last_h2d_bytes`` records the
+        input bytes moved to the device."""
         if A.is_cuda:
             raise ValueError("evaluate_host takes a CPU tensor")
-        return self._host_pipeline(A, lambda x, r: self.evaluate(x, method=method, result=r), chunk, result,
-                                   sync)
+        if self.n_out == 0:
+            raise ValueError("no coefficients set")
+        if A.dim() != 2 or A.shape[1] != self.graph.num_seeds:
+            raise ValueError(f"A must be [S, {self.graph.num_seeds}], got {tuple(A.shape)}")
+        A = A.contiguous()
+        if A.dtype not in (torch.complex128, torch.complex64):
+            raise ValueError("A must be complex128 or complex64")
+        prec = N.PREC_F64 if A.dtype == torch.complex128 else N.PREC_F32
+        S = A.shape[0]
+        kind = N.OUT_COMPLEX if out == "complex" else N.OUT_REAL
+        dt = torch.complex128 if kind == N.OUT_COMPLEX else torch.float64
+        shape = (S,) if self.n_out == 1 else (S, self.n_out)
+        if result is None:
+            result = torch.empty(shape, dtype=dt, pin_memory=True)
+        elif result.is_cuda or result.dtype != dt or tuple(result.shape) != shape or not result.is_contiguous():
+            raise ValueError(f"result must be a contiguous CPU {dt} tensor of shape {shape}")
+        m = N.METHOD_NAIVE if method == "naive" else N.METHOD_RECURSIVE
+        h2d = C.c_int64()
+        dev = torch.device("cuda", self.device)
+        N.check(N.lib().acedag_eval_host(self._h, m, prec, kind, _vp(A), S, _vp(result), C.byref(h2d),
+                                         _stream(dev)))
+        self.last_h2d_bytes = h2d.value
+        return result
 
     def evaluate_positions_host(self, xyz: torch.Tensor, r_in: float = R_IN, r_cut: float = R_CUT,
                                 chunk: int = 65536, result: torch.Tensor | None = None,

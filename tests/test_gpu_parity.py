@@ -249,12 +249,35 @@ def test_host_pipelines_match_device(cuda, cfg2, golden):
     plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
     A = torch.from_numpy(seeded_A(70_000, cfg2.num_seeds, 31))
     dev_phi = plan.evaluate(A.to(cuda)).cpu()
-    host_phi = plan.evaluate_host(A.pin_memory(), chunk=16384)
-    torch.cuda.synchronize()
+    host_phi = plan.evaluate_host(A.pin_memory())
+    assert plan.last_h2d_bytes == 70_000 * plan.info()["used_seeds"] * 16  # used columns only
     assert torch.equal(dev_phi, host_phi)
+    assert torch.equal(dev_phi, plan.evaluate_host(A))  # pageable: row-chunk copies
+    assert plan.last_h2d_bytes == A.numel() * 16
     xyz = torch.from_numpy(golden("positions_cfg3.npz")["xyz"])
     assert torch.equal(plan.evaluate_positions(xyz.to(cuda)).cpu(),
                        plan.evaluate_positions_host(xyz.pin_memory(), chunk=2).clone())
+
+
+def test_eval_host_variants(cuda, cfg2):
+    """acedag_eval_host for the naive method, fp32 mode, several outputs and
+    complex output agrees bit for bit with acedag_eval on the device."""
+    rng = np.random.default_rng(32)
+    A = torch.from_numpy(seeded_A(5_000, cfg2.num_seeds, 33))
+    Ad = A.to(cuda)
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=rng.normal(size=len(cfg2.target_ids)))
+    assert torch.equal(plan.evaluate(Ad, method="naive").cpu(), plan.evaluate_host(A.pin_memory(), method="naive"))
+    A32 = A.to(torch.complex64)
+    assert torch.equal(plan.evaluate(A32.to(cuda)).cpu(), plan.evaluate_host(A32.pin_memory()))
+    assert plan.last_h2d_bytes == 5_000 * plan.info()["used_seeds"] * 8
+    C = rng.normal(size=(len(cfg2.target_ids), 3)) + 1j * rng.normal(size=(len(cfg2.target_ids), 3))
+    plan3 = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=C)
+    Ap = A.pin_memory()
+    assert torch.equal(plan3.evaluate(Ad, out="complex").cpu(), plan3.evaluate_host(Ap, out="complex"))
+    res = torch.empty(5_000, 3, dtype=torch.float64)
+    plan3.evaluate_host(Ap, result=res)
+    assert torch.equal(plan3.evaluate(Ad).cpu(), res)
+    assert plan3.evaluate_host(Ap[:0]).shape == (0, 3)
 
 
 @pytest.mark.parametrize("env", [{"ACEDAG_K2_SPL": "1"}, {"ACEDAG_K2_SPL": "1", "ACEDAG_K2_WARPS": "16"},

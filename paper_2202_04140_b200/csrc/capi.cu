@@ -394,7 +394,7 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   DevGuard dg(P->device);
   try {
     compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, plan_chunks(), P->host,
-                 k2_mode() == 4 ? dev::kTmemRows2 : kTmemRows);
+                 k2_mode() >= 4 ? dev::kTmemRows2 : kTmemRows);
   } catch (const std::domain_error& e) {
     return fail(ACEDAG_ENOTTARGET, e.what());
   } catch (const std::bad_alloc&) {
@@ -613,8 +613,9 @@ int k2_mode() {
     if (e && std::string(e) == "one") return 1;
     if (e && std::string(e) == "tmem") return 3;
     if (e && std::string(e) == "tmem2") return 4;
+    if (e && std::string(e) == "tmem3") return 5;
     if (k2_spl_env() == 1) return 1;
-    return 4;  // measured fastest at cfg2 (profiles/r01)
+    return 5;  // measured fastest at cfg2 and cfg4 (profiles/r01)
   }();
   return m;
 }
@@ -674,6 +675,26 @@ cudaError_t launch_tmem2_w(acedag_plan* P, const double2* A, int64_t S, int L, c
 }
 
 template <int NU, bool HYB>
+cudaError_t launch_tmem3_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                           double* out, const Launch& lc, cudaStream_t st) {
+  constexpr int W = 32;
+  auto k = dev::k2_tmem3<NU, W, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  e = lc.ws->part.alloc((size_t)lc.grid * W * 64);
+  if (e != cudaSuccess) return e;
+  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
+                                        out, lc.ws->gcache.p, lc.ws->part.p);
+  return cudaGetLastError();
+}
+
+template <int NU> struct Tmem3F64 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_tmem3_k<NU, true>(a...) : launch_tmem3_k<NU, false>(a...);
+  }
+};
+
+template <int NU, bool HYB>
 cudaError_t launch_tmem2_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
                            double* out, const Launch& lc, cudaStream_t st) {
   if (lc.block == 32 * 32) {
@@ -686,15 +707,16 @@ cudaError_t launch_tmem2_k(acedag_plan* P, const double2* A, int64_t S, int L, c
   return launch_tmem2_w<NU, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
 }
 
-// geometry of k2_tmem2: 64-site tiles, 64 hot rows in TMEM, 1 KB cold rows
+// geometry of k2_tmem2/3: 64-site tiles, 64 hot rows in TMEM, 1 KB cold rows
 int tmem2_launch(acedag_plan* P, int64_t S, Launch& lc) {
   const int64_t ntiles = (S + 63) / 64;
-  const int warps = k2_warps();
+  const bool v3 = k2_mode() == 5;
+  const int warps = v3 ? 32 : k2_warps();
   lc.block = warps * 32;
   lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
   lc.rows = P->U + 1;
   const int cold = std::max(0, lc.rows - (int)dev::kTmemRows2);
-  const size_t fixed = (size_t)warps * 1024 + 16;
+  const size_t fixed = (size_t)warps * (v3 ? dev::Ring3::kAlloc : 1024) + 16;
   const int us_max = (int)((P->smem_optin - fixed) / 1024);
   lc.us = std::min(cold, us_max);
   lc.hyb = lc.us < cold;
@@ -897,6 +919,10 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
         if (rc) return rc;
         e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
       }
+    } else if (fast && k2_mode() == 5) {
+      int rc = tmem2_launch(P, S, lc);
+      if (rc) return rc;
+      e = by_order<Tmem3F64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
     } else if (fast && k2_mode() == 4) {
       int rc = tmem2_launch(P, S, lc);
       if (rc) return rc;
@@ -1075,6 +1101,7 @@ const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, 
   if (prec == ACEDAG_PREC_F32) return k2_spl() == 2 ? "k2_fast2 (fp32)" : "k2_fast (fp32)";
   if (fast) {
     switch (k2_mode()) {
+      case 5: return "k2_tmem3";
       case 4: return "k2_tmem2";
       case 3: return "k2_tmem";
       case 2: return "k2_fast2";

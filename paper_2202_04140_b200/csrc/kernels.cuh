@@ -752,6 +752,246 @@ k2_tmem2(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
 }
 
+// --------------------------- K2 (TMEM hot seeds, async program ring, v3)
+// k2_tmem2 with a cheaper program stream: each warp's ring is three 32-record
+// slots filled by cp.async one block ahead (no staging registers), records
+// are addressed through a running shared-memory pointer with immediate
+// offsets (two mirrored records after the last slot keep a two-record
+// look-ahead contiguous), and block crossings are detected by a countdown.
+struct Ring3 {
+  static constexpr uint32_t kSlotBytes = 32 * 16, kBytes = 3 * kSlotBytes, kAlloc = kBytes + 2 * 16;
+  const int4* g;     // next block to fetch
+  const int4* gend;  // end of the chunk
+  uint32_t p;        // shared address of the current record
+  uint32_t base;     // shared address of slot 0
+  int left;          // records left in the current block
+  uint32_t nslot;    // slot the next fetched block goes to
+  uint32_t i, n;     // records consumed, chunk length
+
+  __device__ __forceinline__ void fetch(uint32_t slot, int lane) {
+    const int4* src = g + lane;
+    const bool ok = src < gend;
+    const uint32_t sz = ok ? 16u : 0u;
+    const int4* s = ok ? src : g;
+    const uint32_t dst = base + slot * kSlotBytes + lane * 16;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(s), "r"(sz) : "memory");
+    if (slot == 0 && lane < 2)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(base + kBytes + lane * 16), "l"(s),
+                   "r"(sz)
+                   : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    g += 32;
+  }
+  __device__ __forceinline__ void begin(const int4* gp, uint32_t len, uint32_t ring, int lane) {
+    __syncwarp();  // the previous chunk's reads of this ring are done
+    g = gp;
+    gend = gp + len;
+    base = ring;
+    p = ring;
+    left = 32;
+    i = 0;
+    n = len;
+    fetch(0, lane);
+    fetch(1, lane);
+    fetch(2, lane);
+    nslot = 0;
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncwarp();
+  }
+  __device__ __forceinline__ int4 at(uint32_t j) const {
+    int4 r;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(p + j * 16));
+    return r;
+  }
+  __device__ __forceinline__ void advance(uint32_t k, int lane) {  // k <= 2
+    p += k * 16;
+    i += k;
+    left -= (int)k;
+    if (left <= 0) {
+      left += 32;
+      if (p >= base + kBytes) p -= kBytes;
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncwarp();
+      fetch(nslot, lane);
+      nslot = nslot == 2 ? 0 : nslot + 1;
+    }
+  }
+};
+
+template <bool HOT, int K, bool HYB>
+__device__ __forceinline__ void leaf_block_t3(const Ring3& st, double2 pa, double2 pb, double& acc0, double& acc1,
+                                              const SeedsT2<HYB>& sd) {
+  int4 r[K];
+  double2 sa[K], sb[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
+  if constexpr (HOT) {
+    uint32_t t[K][8];
+#pragma unroll
+    for (int j = 0; j < K; ++j) sd.hot_issue((uint32_t)r[j].z, t[j]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      sa[j] = make_double2(__hiloint2double(t[j][1], t[j][0]), __hiloint2double(t[j][3], t[j][2]));
+      sb[j] = make_double2(__hiloint2double(t[j][5], t[j][4]), __hiloint2double(t[j][7], t[j][6]));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) sd.cold((uint32_t)r[j].z, sa[j], sb[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double c = rec_c(r[j]);
+    acc0 += c * (sa[j].x * pa.x - sa[j].y * pa.y);
+    acc1 += c * (sb[j].x * pb.x - sb[j].y * pb.y);
+  }
+}
+
+template <bool HOT, bool HYB>
+__device__ __forceinline__ void leaves_t3(Ring3& st, uint32_t n, double2 pa, double2 pb, double& acc0, double& acc1,
+                                          const SeedsT2<HYB>& sd, int lane) {
+  for (; n >= 2; n -= 2) {
+    leaf_block_t3<HOT, 2, HYB>(st, pa, pb, acc0, acc1, sd);
+    st.advance(2, lane);
+  }
+  if (n) {
+    leaf_block_t3<HOT, 1, HYB>(st, pa, pb, acc0, acc1, sd);
+    st.advance(1, lane);
+  }
+}
+
+template <int D, int NU, bool HYB>
+__device__ __forceinline__ void k2t3_visit(Ring3& st, uint32_t n, uint32_t nh, double2 pa, double2 pb,
+                                           double& acc0, double& acc1, const SeedsT2<HYB>& sd, int lane) {
+  if constexpr (D > NU) {
+    return;
+  } else if constexpr (D == NU) {
+    leaves_t3<true, HYB>(st, nh, pa, pb, acc0, acc1, sd, lane);
+    leaves_t3<false, HYB>(st, n - nh, pa, pb, acc0, acc1, sd, lane);
+  } else {
+    for (uint32_t j = 0; j < n; ++j) {
+      const int4 r = st.at(0);
+      st.advance(1, lane);
+      double2 sa, sb;
+      sd.get((uint32_t)r.z, j < nh, sa, sb);
+      const double2 va = cmul(sa, pa), vb = cmul(sb, pb);
+      const double c = rec_c(r);
+      acc0 += c * va.x;
+      acc1 += c * vb.x;
+      k2t3_visit<D + 1, NU, HYB>(st, rec_nch(r), (uint32_t)r.w >> 16, va, vb, acc0, acc1, sd, lane);
+    }
+  }
+}
+
+template <int NU, int WARPS, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
+         int Us_cold, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
+         double* __restrict__ out, double2* __restrict__ gcache, double* __restrict__ part) {
+  unsigned char* smem = g_smem;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rows = U + 1;
+  const int hot = rows < (int)kTmemRows2 ? rows : (int)kTmemRows2;
+  const int cold = rows - hot;
+  const int us = cold < Us_cold ? cold : Us_cold;
+  double2* sC = reinterpret_cast<double2*>(smem);  // [us][64]
+  const uint32_t rings = (uint32_t)((size_t)us * 1024);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + rings + WARPS * Ring3::kAlloc);
+  double2* gC = HYB ? gcache + (size_t)blockIdx.x * (cold - us) * 64 : nullptr;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tbase = *tslot;
+  SeedsT2<HYB> sd;
+  sd.tq = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+  sd.s = (uint32_t)(lane * 16);
+  sd.g = HYB ? reinterpret_cast<const char*>(gC) + lane * 16 : nullptr;
+  sd.us_rows = (uint32_t)us;
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem + rings + warp * Ring3::kAlloc);
+  double* mypart = part + (size_t)blockIdx.x * WARPS * 64;
+  Ring3 st;
+  const int64_t ntiles = (S + 63) / 64;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t sa_i = tile * 64 + lane, sb_i = sa_i + 32;
+    const bool va_ok = sa_i < S, vb_ok = sb_i < S;
+    const double2* rowa = A + (va_ok ? sa_i : 0) * (int64_t)L;
+    const double2* rowb = A + (vb_ok ? sb_i : 0) * (int64_t)L;
+    for (int h = warp >> 2; h < hot; h += WARPS / 4) {
+      double2 a, b;
+      if (h == U) {
+        a = b = make_double2(1.0, 0.0);
+      } else {
+        const int lab = __ldg(slot_label + h);
+        a = va_ok ? ld_stream(rowa + lab) : make_double2(0.0, 0.0);
+        b = vb_ok ? ld_stream(rowb + lab) : make_double2(0.0, 0.0);
+      }
+      tmem_st8(sd.tq + (uint32_t)h * 8, a, b);
+    }
+    for (int c = warp; c < cold; c += WARPS) {
+      const int u = hot + c;
+      double2 a, b;
+      if (u == U) {
+        a = b = make_double2(1.0, 0.0);
+      } else {
+        const int lab = __ldg(slot_label + u);
+        a = va_ok ? ld_stream(rowa + lab) : make_double2(0.0, 0.0);
+        b = vb_ok ? ld_stream(rowb + lab) : make_double2(0.0, 0.0);
+      }
+      if (!HYB || c < us) {
+        sC[c * 64 + lane] = a;
+        sC[c * 64 + 32 + lane] = b;
+      } else {
+        gC[(size_t)(c - us) * 64 + lane] = a;
+        gC[(size_t)(c - us) * 64 + 32 + lane] = b;
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    double wa = 0.0, wb = 0.0;
+    for (int ci = warp; ci < nchunk; ci += WARPS) {
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), ring, lane);
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        st.advance(2, lane);
+        const uint32_t fl = (uint32_t)r1.w >> 16;
+        double2 a0, b0, a1, b1;
+        sd.get((uint32_t)r0.z, fl & 1u, a0, b0);
+        sd.get((uint32_t)r1.z, (fl >> 1) & 1u, a1, b1);
+        const double2 va = cmul(a0, a1), vb = cmul(b0, b1);
+        const double c = rec_c(r0);
+        wa += c * va.x;
+        wb += c * vb.x;
+        k2t3_visit<3, NU, HYB>(st, rec_nch(r0), (uint32_t)r0.w >> 16, va, vb, wa, wb, sd, lane);
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    mypart[(warp * 2 + 0) * 32 + lane] = wa;
+    mypart[(warp * 2 + 1) * 32 + lane] = wb;
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (warp < 2) {
+      double s = 0.0;
+      for (int w = 0; w < WARPS; ++w) s += __ldcg(mypart + (w * 2 + warp) * 32 + lane);
+      const int64_t site = tile * 64 + warp * 32 + lane;
+      if (site < S) out[site] = s;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
 // ------------------------------------------------------ K2 (two sites/lane)
 // 64-site tiles: lane handles sites t*64 + lane and t*64 + 32 + lane, so each
 // program record (and its decode) serves twice the sites.  The seed table is

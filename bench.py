@@ -452,7 +452,7 @@ def run_ours(a):
                                + "; MEASURED_PEAKS.json has no FP64 entry",
                 "flops_per_site": F,
                 "flop_model": "F_site = 6 P_int + 3 L_f + 2 T n_out" + (" + 4 J U_used" if pos else "") + " (SURVEY.md 8d)"}
-    roof["kernel"] = plan.kernel_name(prec=a.prec)
+    roof["kernel"] = plan.kernel_name(prec=a.prec, sites=S)
     roof["kernel_ms"] = k2_ms
     prof = os.path.join(ROOT, "profiles", "r01", "traffic.json")
     roof["traffic"] = None

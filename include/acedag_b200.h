@@ -137,10 +137,10 @@ int acedag_plan_program(const acedag_graph* g, const int64_t* node_ids,
                         int64_t* n_slots, void* ops, int64_t* n_ops,
                         int32_t* chunk, int64_t* stats);
 
-/* Name of the kernel acedag_eval would launch for these arguments (static
- * string; "" and EINVAL on bad arguments).  For reporting only. */
+/* Name of the kernel acedag_eval would launch for these arguments and S
+ * sites (static string; "" and EINVAL on bad arguments).  For reporting. */
 const char* acedag_eval_kernel_name(const acedag_plan* plan, int method, int prec,
-                                    int out_kind);
+                                    int out_kind, int64_t S);
 
 /* phi for S sites: replaces evaluate_graph + sum(c * v) (evaluator.py:93-110,
  * 141-142) [method RECURSIVE] or sum(c * naive_eval) (evaluator.py:113-121)

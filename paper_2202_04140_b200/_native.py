@@ -45,7 +45,7 @@ SIGNATURES = {
                                        _vp, _i64p, _i32p, _i64p]),
     "acedag_plan_info": (C.c_int, [_vp, _i64p, _i64p, _i64p, _i64p]),
     "acedag_eval": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, _vp]),
-    "acedag_eval_kernel_name": (C.c_char_p, [_vp, C.c_int, C.c_int, C.c_int]),
+    "acedag_eval_kernel_name": (C.c_char_p, [_vp, C.c_int, C.c_int, C.c_int, C.c_int64]),
     "acedag_naive_products": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp, _vp]),
     "acedag_reduce_sites": (C.c_int, [_vp, _vp, C.c_int64, _vp, _vp]),
     "acedag_eval_nodes": (C.c_int, [_vp, _vp, C.c_int64, _vp, _vp]),

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -181,6 +182,90 @@ namespace {
 int k2_mode();  // fp64 fast-path kernel selection (below)
 }
 
+namespace {
+// Program re-encoding for k2_tmem4 (kernels.cuh, Op4 comment): seed locators
+// per class (TMEM column / shared / global-cache byte offset) and per node the
+// counts of children in each class (children are slot-ordered by the plan).
+// Returns false if a count does not fit the packed word.
+bool encode_ops4(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<Op>& o4, std::vector<int32_t>& croots) {
+  o4 = H.ops;
+  auto cls = [&](uint32_t s) { return s < hot ? 0u : (s < hot + us ? 1u : 2u); };
+  auto loc = [&](uint32_t s) { return s < hot ? s * 8u : (s < hot + us ? (s - hot) * 1024u : (s - hot - us) * 1024u); };
+  auto setw = [&](size_t i, uint32_t w) {
+    o4[i].nch = (uint16_t)(w & 0xFFFFu);
+    o4[i].skip = (uint16_t)(w >> 16);
+  };
+  bool ok = true;
+  std::function<size_t(size_t, uint32_t, uint32_t&, uint32_t&)> walk = [&](size_t pos, uint32_t n, uint32_t& nh,
+                                                                            uint32_t& ns) -> size_t {
+    nh = ns = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+      const size_t me = pos;
+      const uint32_t s = H.ops[me].off / kRowBytes, c = cls(s);
+      nh += c == 0;
+      ns += c == 1;
+      o4[me].off = loc(s);
+      uint32_t h2, s2;
+      const uint32_t ch = H.ops[me].nch;
+      pos = walk(me + 1, ch, h2, s2);
+      if (ch > 0x7FFu || h2 > 0x7FFu || s2 > 0x3FFu) ok = false;
+      setw(me, ch | h2 << 11 | s2 << 22);
+    }
+    return pos;
+  };
+  croots.assign(H.chunk.size() - 1, 0);
+  for (size_t ci = 0; ci + 1 < H.chunk.size(); ++ci) {
+    size_t i = (size_t)H.chunk[ci];
+    while (i < (size_t)H.chunk[ci + 1]) {
+      croots[ci]++;
+      const uint32_t sa = H.ops[i].off / kRowBytes, sb = H.ops[i + 1].off / kRowBytes;
+      o4[i].off = loc(sa);
+      o4[i + 1].off = loc(sb);
+      setw(i + 1, cls(sa) | cls(sb) << 2);
+      uint32_t nh, ns;
+      const uint32_t ch = H.ops[i].nch;
+      const size_t end = walk(i + 2, ch, nh, ns);
+      if (ch > 0x7FFu || nh > 0x7FFu || ns > 0x3FFu) ok = false;
+      setw(i, ch | nh << 11 | ns << 22);
+      i = end;
+    }
+  }
+  return ok;
+}
+}  // namespace
+
+namespace {
+// The same program with a smaller TMEM-resident set (k2_quad keeps the 32
+// hottest slots): per node, the count of leading children whose slot is
+// below `hot`, and a root's hot flags.  Needs slot-ordered children (plan).
+std::vector<Op> reencode_hot(const PlanHost& H, uint32_t hot) {
+  std::vector<Op> o = H.ops;
+  std::function<size_t(size_t, uint32_t, uint32_t&)> walk = [&](size_t pos, uint32_t n, uint32_t& nh) -> size_t {
+    nh = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+      const size_t me = pos;
+      nh += H.ops[me].off / kRowBytes < hot;
+      uint32_t h2;
+      pos = walk(me + 1, H.ops[me].nch, h2);
+      o[me].skip = (uint16_t)h2;
+    }
+    return pos;
+  };
+  for (size_t ci = 0; ci + 1 < H.chunk.size(); ++ci) {
+    size_t i = (size_t)H.chunk[ci];
+    while (i < (size_t)H.chunk[ci + 1]) {
+      const uint32_t sa = H.ops[i].off / kRowBytes, sb = H.ops[i + 1].off / kRowBytes;
+      o[i + 1].skip = (uint16_t)((sa < hot ? 1 : 0) | (sb < hot ? 2 : 0));
+      uint32_t nh;
+      const size_t end = walk(i + 2, H.ops[i].nch, nh);
+      o[i].skip = (uint16_t)nh;
+      i = end;
+    }
+  }
+  return o;
+}
+}  // namespace
+
 struct acedag_graph {
   Graph g;
 };
@@ -203,6 +288,10 @@ struct acedag_plan {
   DevBuf<int32_t> col_of;  // label -> seed slot or -1 (pool of used labels only)
   DevBuf<int4> tri;        // (n, l, m >= 0) triples the used labels need
   DevBuf<Op> ops;
+  DevBuf<Op> opsQ;         // k2_quad: hot counts for its 32 TMEM slots
+  DevBuf<Op> ops4;         // k2_tmem4 encoding (encode_ops4), if it fits
+  DevBuf<int32_t> croots;  // roots per chunk
+  bool ops4_ok = false;
   DevBuf<int32_t> chunk;
   DevBuf<double> cre, cim;
   DevBuf<int32_t> nseg;
@@ -211,6 +300,7 @@ struct acedag_plan {
   // per-stream scratch (seed cold tails, chunk partials, pooled A): calls on
   // distinct streams may run concurrently
   struct Workspace {
+    DevBuf<double> tail;  // split last-round partials
     DevBuf<double2> gcache;
     DevBuf<double2> ws_A;
     DevBuf<double> part;  // K2 partial sums
@@ -247,6 +337,18 @@ struct acedag_plan {
     return w.get();
   }
 };
+
+namespace {
+// shared-memory cold rows of k2_tmem3/4 (32 warps, 3-slot program rings)
+int tmem_us_max(const acedag_plan* P) {
+  const size_t fixed = (size_t)32 * dev::Ring3::kAlloc + 16;
+  return (int)((P->smem_optin - fixed) / 1024);
+}
+int tmem_us_max_clamped(const acedag_plan* P) {
+  const int cold = std::max(0, P->U + 1 - (int)dev::kTmemRows2);
+  return std::min(cold, tmem_us_max(P));
+}
+}  // namespace
 
 // ====================================================================== API
 extern "C" {
@@ -431,6 +533,17 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   }
   CK(P->ops.upload(H.ops));
   CK(P->chunk.upload(H.chunk));
+  if (k2_mode() == 5 || k2_mode() == 7) CK(P->opsQ.upload(reencode_hot(H, dev::kTmemRowsQ)));
+  if (k2_mode() == 6) {
+    const int rows = P->U + 1, cold = std::max(0, rows - (int)dev::kTmemRows2);
+    std::vector<Op> o4;
+    std::vector<int32_t> cr;
+    P->ops4_ok = encode_ops4(H, dev::kTmemRows2, (uint32_t)std::min(cold, tmem_us_max(P)), o4, cr);
+    if (P->ops4_ok) {
+      CK(P->ops4.upload(o4));
+      CK(P->croots.upload(cr));
+    }
+  }
   {
     std::vector<double> padded(H.cre);
     // k2_multi reads whole 32-output slices; k2_mma prefetches two 4-record
@@ -529,6 +642,12 @@ int k2_warps() {
   return w;
 }
 
+// auto selection (k2_mode 5): four sites per lane pays off where the program
+// is order <= 4 (k2_quad spills deeper) and the sites fill a round of tiles
+bool use_quad(const acedag_plan* P, int64_t S) {
+  return P->host.max_order <= 4 && (S + 127) / 128 >= P->sms - t_sm_reserve;
+}
+
 // tile geometry: 32 sites per CTA, seed rows [Us][32] in smem (U used seeds
 // plus the constant ONE row), the tail in the per-CTA global cache
 int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, int warps, Launch& lc,
@@ -606,6 +725,9 @@ int k2_maxu() {
 // fp64 fast-path kernel: "tmem2" (default: two sites per lane, hot seeds in
 // tensor memory), "tmem" (one site per lane, hot seeds in TMEM), "two" (two
 // sites per lane, shared memory only), "one"; ACEDAG_K2 overrides
+// fp64 single-output kernel: ACEDAG_K2 = one | two | tmem | tmem2 | tmem3 |
+// tmem4 | quad; default "auto" = k2_quad for order <= 4 when the sites fill
+// at least one round of 128-site tiles, else k2_tmem3 (profiles/r01)
 int k2_mode() {
   static int m = [] {
     const char* e = getenv("ACEDAG_K2");
@@ -613,9 +735,11 @@ int k2_mode() {
     if (e && std::string(e) == "one") return 1;
     if (e && std::string(e) == "tmem") return 3;
     if (e && std::string(e) == "tmem2") return 4;
-    if (e && std::string(e) == "tmem3") return 5;
+    if (e && std::string(e) == "tmem4") return 6;
+    if (e && std::string(e) == "quad") return 7;
+    if (e && std::string(e) == "tmem3") return 8;
     if (k2_spl_env() == 1) return 1;
-    return 5;  // measured fastest at cfg2 and cfg4 (profiles/r01)
+    return 5;
   }();
   return m;
 }
@@ -674,6 +798,26 @@ cudaError_t launch_tmem2_w(acedag_plan* P, const double2* A, int64_t S, int L, c
   return cudaGetLastError();
 }
 
+// The last round of a persistent tile loop is short of tiles when ntiles is
+// not a multiple of the grid; those tiles are split into `parts` program
+// slices (up to the grid, at most ACEDAG_TAIL_PARTS, default 8) whose partial
+// sums are added in slice order.  full = tiles run whole.
+void tail_split(int64_t ntiles, int grid, int nchunk, int64_t& full, int& parts) {
+  static int cap = [] {
+    const char* e = getenv("ACEDAG_TAIL_PARTS");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  const int64_t rem = ntiles % grid;
+  full = ntiles;
+  parts = 1;
+  if (rem == 0) return;
+  int p = (int)std::min<int64_t>(grid / rem, cap);
+  p = std::min(p, std::max(1, nchunk / 8));
+  if (p <= 1) return;
+  full = ntiles - rem;
+  parts = p;
+}
+
 template <int NU, bool HYB>
 cudaError_t launch_tmem3_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
                            double* out, const Launch& lc, cudaStream_t st) {
@@ -681,10 +825,22 @@ cudaError_t launch_tmem3_k(acedag_plan* P, const double2* A, int64_t S, int L, c
   auto k = dev::k2_tmem3<NU, W, HYB>;
   cudaError_t e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
-  e = lc.ws->part.alloc((size_t)lc.grid * W * 64);
+  e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 64);
   if (e != cudaSuccess) return e;
+  const int64_t ntiles = (S + 63) / 64;
+  int64_t full = ntiles;
+  int parts = 1;
+  tail_split(ntiles, lc.grid, nchunks(P), full, parts);
+  if (parts > 1) {
+    e = lc.ws->tail.alloc((size_t)(ntiles - full) * nchunks(P) * 64);
+    if (e != cudaSuccess) return e;
+  }
   k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p);
+                                        out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || parts == 1) return e;
+  const int64_t rem = S - full * 64;
+  dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 64, S, 64, nchunks(P), out);
   return cudaGetLastError();
 }
 
@@ -707,10 +863,80 @@ cudaError_t launch_tmem2_k(acedag_plan* P, const double2* A, int64_t S, int L, c
   return launch_tmem2_w<NU, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
 }
 
-// geometry of k2_tmem2/3: 64-site tiles, 64 hot rows in TMEM, 1 KB cold rows
+template <int NU, bool HYB>
+cudaError_t launch_tmem4_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                           double* out, const Launch& lc, cudaStream_t st) {
+  constexpr int W = 32;
+  auto k = dev::k2_tmem4<NU, W, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  e = lc.ws->part.alloc((size_t)lc.grid * W * 64);
+  if (e != cudaSuccess) return e;
+  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops4.p, P->chunk.p, P->croots.p,
+                                        nchunks(P), out, lc.ws->gcache.p, lc.ws->part.p);
+  return cudaGetLastError();
+}
+
+template <int NU, bool HYB>
+cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                          double* out, const Launch& lc, cudaStream_t st) {
+  constexpr int W = 16;
+  const bool two = getenv("ACEDAG_K2_MAXU") ? k2_maxu() >= 2 : NU <= 4;
+  auto k = two ? dev::k2_quad<NU, W, 2, HYB> : dev::k2_quad<NU, W, 1, HYB>;
+  cudaError_t e = set_smem(k, lc.smem);
+  if (e != cudaSuccess) return e;
+  e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 128);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (S + 127) / 128;
+  int64_t full = ntiles;
+  int parts = 1;
+  tail_split(ntiles, lc.grid, nchunks(P), full, parts);
+  if (parts > 1) {
+    e = lc.ws->tail.alloc((size_t)(ntiles - full) * nchunks(P) * 128);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->opsQ.p, P->chunk.p, nchunks(P),
+                                        out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || parts == 1) return e;
+  const int64_t rem = S - full * 128;
+  dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 128, S, 128, nchunks(P), out);
+  return cudaGetLastError();
+}
+
+template <int NU> struct QuadF64 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_quad_k<NU, true>(a...) : launch_quad_k<NU, false>(a...);
+  }
+};
+
+// geometry of k2_quad: 128-site tiles, 32 hot rows in TMEM, 2 KB cold rows
+int quad_launch(acedag_plan* P, int64_t S, Launch& lc) {
+  const int64_t ntiles = (S + 127) / 128;
+  lc.block = 16 * 32;
+  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
+  lc.rows = P->U + 1;
+  const int cold = std::max(0, lc.rows - (int)dev::kTmemRowsQ);
+  const size_t fixed = (size_t)16 * dev::Ring3::kAlloc + 16;
+  const int us_max = (int)((P->smem_optin - fixed) / 2048);
+  lc.us = std::min(cold, us_max);
+  lc.hyb = lc.us < cold;
+  lc.smem = (size_t)lc.us * 2048 + fixed;
+  if (lc.hyb && lc.ws->gcache.alloc((size_t)lc.grid * (cold - lc.us) * 128) != cudaSuccess)
+    return fail(ACEDAG_ENOMEM, "gcache allocation failed");
+  return 0;
+}
+
+template <int NU> struct Tmem4F64 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_tmem4_k<NU, true>(a...) : launch_tmem4_k<NU, false>(a...);
+  }
+};
+
+// geometry of k2_tmem2/3/4: 64-site tiles, 64 hot rows in TMEM, 1 KB cold rows
 int tmem2_launch(acedag_plan* P, int64_t S, Launch& lc) {
   const int64_t ntiles = (S + 63) / 64;
-  const bool v3 = k2_mode() == 5;
+  const bool v3 = k2_mode() >= 5 && k2_mode() != 7;
   const int warps = v3 ? 32 : k2_warps();
   lc.block = warps * 32;
   lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
@@ -919,7 +1145,16 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
         if (rc) return rc;
         e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
       }
-    } else if (fast && k2_mode() == 5) {
+    } else if (fast && (k2_mode() == 7 || (k2_mode() == 5 && use_quad(P, S)))) {
+      int rc = quad_launch(P, S, lc);
+      if (rc) return rc;
+      e = by_order<QuadF64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
+    } else if (fast && k2_mode() == 6 && P->ops4_ok) {
+      int rc = tmem2_launch(P, S, lc);
+      if (rc) return rc;
+      if (lc.us != tmem_us_max_clamped(P)) return fail(ACEDAG_EINVAL, "k2_tmem4 geometry mismatch");
+      e = by_order<Tmem4F64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
+    } else if (fast && (k2_mode() == 5 || k2_mode() == 8 || k2_mode() == 6)) {
       int rc = tmem2_launch(P, S, lc);
       if (rc) return rc;
       e = by_order<Tmem3F64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
@@ -1090,7 +1325,7 @@ int acedag_eval_host(const acedag_plan* Pc, int method, int prec, int out_kind, 
   return ACEDAG_OK;
 }
 
-const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, int out_kind) {
+const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, int out_kind, int64_t S) {
   if (!P || !P->has_coef) {
     fail(ACEDAG_EINVAL, "plan has no coefficients");
     return "";
@@ -1101,7 +1336,10 @@ const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, 
   if (prec == ACEDAG_PREC_F32) return k2_spl() == 2 ? "k2_fast2 (fp32)" : "k2_fast (fp32)";
   if (fast) {
     switch (k2_mode()) {
-      case 5: return "k2_tmem3";
+      case 8: return "k2_tmem3";
+      case 7: return "k2_quad";
+      case 6: return P->ops4_ok ? "k2_tmem4" : "k2_tmem3";
+      case 5: return use_quad(P, S) ? "k2_quad" : "k2_tmem3";
       case 4: return "k2_tmem2";
       case 3: return "k2_tmem";
       case 2: return "k2_fast2";

@@ -26,9 +26,13 @@ template <typename T> struct V2;
 template <> struct V2<double> { using t = double2; };
 template <> struct V2<float> { using t = float2; };
 
+// fp64 products with a fixed contraction (explicit FMAs), so every kernel
+// geometry computes the same value for a site
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
+// Re(s * p)
+__device__ __forceinline__ double re_mul(double2 s, double2 p) { return __fma_rn(s.x, p.x, -__dmul_rn(s.y, p.y)); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -844,8 +848,8 @@ __device__ __forceinline__ void leaf_block_t3(const Ring3& st, double2 pa, doubl
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const double c = rec_c(r[j]);
-    acc0 += c * (sa[j].x * pa.x - sa[j].y * pa.y);
-    acc1 += c * (sb[j].x * pb.x - sb[j].y * pb.y);
+    acc0 = __fma_rn(c, re_mul(sa[j], pa), acc0);
+    acc1 = __fma_rn(c, re_mul(sb[j], pb), acc1);
   }
 }
 
@@ -878,8 +882,8 @@ __device__ __forceinline__ void k2t3_visit(Ring3& st, uint32_t n, uint32_t nh, d
       sd.get((uint32_t)r.z, j < nh, sa, sb);
       const double2 va = cmul(sa, pa), vb = cmul(sb, pb);
       const double c = rec_c(r);
-      acc0 += c * va.x;
-      acc1 += c * vb.x;
+      acc0 = __fma_rn(c, va.x, acc0);
+      acc1 = __fma_rn(c, vb.x, acc1);
       k2t3_visit<D + 1, NU, HYB>(st, rec_nch(r), (uint32_t)r.w >> 16, va, vb, acc0, acc1, sd, lane);
     }
   }
@@ -889,7 +893,8 @@ template <int NU, int WARPS, bool HYB>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
          int Us_cold, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
-         double* __restrict__ out, double2* __restrict__ gcache, double* __restrict__ part) {
+         double* __restrict__ out, double2* __restrict__ gcache, double* __restrict__ part, int64_t full_tiles,
+         int tail_parts, double* __restrict__ tailbuf) {
   unsigned char* smem = g_smem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rows = U + 1;
@@ -915,8 +920,306 @@ k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
   sd.g = HYB ? reinterpret_cast<const char*>(gC) + lane * 16 : nullptr;
   sd.us_rows = (uint32_t)us;
   const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem + rings + warp * Ring3::kAlloc);
-  double* mypart = part + (size_t)blockIdx.x * WARPS * 64;
+  double* mypart = part + (size_t)blockIdx.x * nchunk * 64;
   Ring3 st;
+  // whole tiles, then the last round's tiles split into program slices (k2_quad)
+  const int64_t ntiles = (S + 63) / 64;
+  const int64_t nitems = full_tiles + (ntiles - full_tiles) * tail_parts;
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const bool whole = it < full_tiles;
+    const int64_t tile = whole ? it : full_tiles + (it - full_tiles) / tail_parts;
+    const int slice = whole ? 0 : (int)((it - full_tiles) % tail_parts);
+    const int nsl = whole ? 1 : tail_parts;
+    const int cb = (int)((int64_t)slice * nchunk / nsl), ce = (int)((int64_t)(slice + 1) * nchunk / nsl);
+    const int64_t sa_i = tile * 64 + lane, sb_i = sa_i + 32;
+    const bool va_ok = sa_i < S, vb_ok = sb_i < S;
+    const double2* rowa = A + (va_ok ? sa_i : 0) * (int64_t)L;
+    const double2* rowb = A + (vb_ok ? sb_i : 0) * (int64_t)L;
+    for (int h = warp >> 2; h < hot; h += WARPS / 4) {
+      double2 a, b;
+      if (h == U) {
+        a = b = make_double2(1.0, 0.0);
+      } else {
+        const int lab = __ldg(slot_label + h);
+        a = va_ok ? ld_stream(rowa + lab) : make_double2(0.0, 0.0);
+        b = vb_ok ? ld_stream(rowb + lab) : make_double2(0.0, 0.0);
+      }
+      tmem_st8(sd.tq + (uint32_t)h * 8, a, b);
+    }
+    for (int c = warp; c < cold; c += WARPS) {
+      const int u = hot + c;
+      double2 a, b;
+      if (u == U) {
+        a = b = make_double2(1.0, 0.0);
+      } else {
+        const int lab = __ldg(slot_label + u);
+        a = va_ok ? ld_stream(rowa + lab) : make_double2(0.0, 0.0);
+        b = vb_ok ? ld_stream(rowb + lab) : make_double2(0.0, 0.0);
+      }
+      if (!HYB || c < us) {
+        sC[c * 64 + lane] = a;
+        sC[c * 64 + 32 + lane] = b;
+      } else {
+        gC[(size_t)(c - us) * 64 + lane] = a;
+        gC[(size_t)(c - us) * 64 + 32 + lane] = b;
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    // one partial per (chunk, site), summed in chunk order: the result is
+    // independent of the warp count, the tail split and the site count
+    double* dst = whole ? mypart : tailbuf + (size_t)((it - full_tiles) / tail_parts) * nchunk * 64;
+    for (int ci = cb + warp; ci < ce; ci += WARPS) {
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), ring, lane);
+      double wa = 0.0, wb = 0.0;
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        st.advance(2, lane);
+        const uint32_t fl = (uint32_t)r1.w >> 16;
+        double2 a0, b0, a1, b1;
+        sd.get((uint32_t)r0.z, fl & 1u, a0, b0);
+        sd.get((uint32_t)r1.z, (fl >> 1) & 1u, a1, b1);
+        const double2 va = cmul(a0, a1), vb = cmul(b0, b1);
+        const double c = rec_c(r0);
+        wa = __fma_rn(c, va.x, wa);
+        wb = __fma_rn(c, vb.x, wb);
+        k2t3_visit<3, NU, HYB>(st, rec_nch(r0), (uint32_t)r0.w >> 16, va, vb, wa, wb, sd, lane);
+      }
+      dst[(size_t)ci * 64 + lane] = wa;
+      dst[(size_t)ci * 64 + 32 + lane] = wb;
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (whole && threadIdx.x < 64) {
+      double s = 0.0;
+#pragma unroll 16
+      for (int ci = 0; ci < nchunk; ++ci) s += __ldcg(mypart + (size_t)ci * 64 + threadIdx.x);
+      const int64_t site = tile * 64 + threadIdx.x;
+      if (site < S) out[site] = s;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
+// ------------------- K2 (TMEM hot seeds, three seed classes per node, v4)
+// k2_tmem3 with the program re-encoded for this kernel (Op4): every node's
+// children are ordered hot (TMEM) / shared-memory / global-cache by seed slot
+// and the record carries the three counts, so each leaf run is three
+// branch-free loops; seed locators are pre-scaled per class (TMEM column,
+// shared byte offset, global byte offset); each chunk's root count bounds the
+// root loop, so the ring keeps no record counter.
+//   w (non-root and a root's first record): nch | nh << 11 | ns << 22
+//   a root's second record w: class of seed a | class of seed b << 2
+struct Ring4 {
+  static constexpr uint32_t kSlotBytes = 32 * 16, kBytes = 3 * kSlotBytes, kAlloc = kBytes + 2 * 16;
+  uint32_t p;   // shared address of the current record
+  int left;     // records left in the current block
+  uint32_t gi;  // next block to fetch (record index)
+  uint32_t ge;  // end of the chunk (record index)
+
+  __device__ __forceinline__ static void fetch(const int4* ops, uint32_t base, uint32_t slot, uint32_t gi,
+                                               uint32_t ge, int lane) {
+    const uint32_t q = gi + lane;
+    const bool ok = q < ge;
+    const int4* s = ops + (ok ? q : gi);
+    const uint32_t sz = ok ? 16u : 0u;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(base + slot * kSlotBytes + lane * 16),
+                 "l"(s), "r"(sz)
+                 : "memory");
+    if (slot == 0 && lane < 2)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(base + kBytes + lane * 16), "l"(s),
+                   "r"(sz)
+                   : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  __device__ __forceinline__ void begin(const int4* ops, uint32_t b, uint32_t e, uint32_t base, int lane) {
+    __syncwarp();
+    p = base;
+    left = 32;
+    ge = e;
+    fetch(ops, base, 0, b, e, lane);
+    fetch(ops, base, 1, b + 32, e, lane);
+    fetch(ops, base, 2, b + 64, e, lane);
+    gi = b + 96;
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncwarp();
+  }
+  __device__ __forceinline__ int4 at(uint32_t j) const {
+    int4 r;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "r"(p + j * 16));
+    return r;
+  }
+  // base: this warp's ring (recomputed by the caller only when crossing)
+  template <typename BaseFn>
+  __device__ __forceinline__ void advance(uint32_t k, const int4* ops, BaseFn base_fn, int lane) {
+    p += k * 16;
+    left -= (int)k;
+    if (left <= 0) {
+      left += 32;
+      const uint32_t base = base_fn();
+      if (p >= base + kBytes) p -= kBytes;
+      // the slot just left is refilled with the block after the next one
+      const uint32_t cur = (p - base) / kSlotBytes;
+      const uint32_t freed = cur == 0 ? 2u : cur - 1;
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncwarp();
+      fetch(ops, base, freed, gi, ge, lane);
+      gi += 32;
+    }
+  }
+};
+
+template <bool HYB>
+struct SeedsT4 {
+  uint32_t tq;      // TMEM address of this warp's quadrant, column 0
+  uint32_t sb;      // shared address of cold row 0, this lane's site A
+  const char* gb;   // global cache of this tile, this lane's site A
+  // class 0: TMEM column; 1: shared byte offset; 2: global byte offset
+  __device__ __forceinline__ void hot_issue(uint32_t col, uint32_t (&t)[8]) const { tmem_ld8(tq + col, t); }
+  __device__ __forceinline__ void smem(uint32_t off, double2& a, double2& b) const {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(a.x), "=d"(a.y) : "r"(sb + off));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(b.x), "=d"(b.y) : "r"(sb + off + 512));
+  }
+  __device__ __forceinline__ void glob(uint32_t off, double2& a, double2& b) const {
+    a = *reinterpret_cast<const double2*>(gb + off);
+    b = *reinterpret_cast<const double2*>(gb + off + 512);
+  }
+  __device__ __forceinline__ void get(uint32_t off, uint32_t cls, double2& a, double2& b) const {
+    if (cls == 0) {
+      uint32_t t[8];
+      hot_issue(off, t);
+      tmem_wait_ld();
+      a = make_double2(__hiloint2double(t[1], t[0]), __hiloint2double(t[3], t[2]));
+      b = make_double2(__hiloint2double(t[5], t[4]), __hiloint2double(t[7], t[6]));
+    } else if (!HYB || cls == 1) {
+      smem(off, a, b);
+    } else {
+      glob(off, a, b);
+    }
+  }
+};
+
+template <int CLS, int K, bool HYB>
+__device__ __forceinline__ void leaf_block_t4(const Ring4& st, double2 pa, double2 pb, double& acc0, double& acc1,
+                                              const SeedsT4<HYB>& sd) {
+  int4 r[K];
+  double2 sa[K], sb[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
+  if constexpr (CLS == 0) {
+    uint32_t t[K][8];
+#pragma unroll
+    for (int j = 0; j < K; ++j) sd.hot_issue((uint32_t)r[j].z, t[j]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      sa[j] = make_double2(__hiloint2double(t[j][1], t[j][0]), __hiloint2double(t[j][3], t[j][2]));
+      sb[j] = make_double2(__hiloint2double(t[j][5], t[j][4]), __hiloint2double(t[j][7], t[j][6]));
+    }
+  } else if constexpr (CLS == 1) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) sd.smem((uint32_t)r[j].z, sa[j], sb[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) sd.glob((uint32_t)r[j].z, sa[j], sb[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double c = rec_c(r[j]);
+    acc0 += c * (sa[j].x * pa.x - sa[j].y * pa.y);
+    acc1 += c * (sb[j].x * pb.x - sb[j].y * pb.y);
+  }
+}
+
+template <int CLS, bool HYB, typename BaseFn>
+__device__ __forceinline__ void leaves_t4(Ring4& st, uint32_t n, double2 pa, double2 pb, double& acc0,
+                                          double& acc1, const SeedsT4<HYB>& sd, const int4* ops, BaseFn bf,
+                                          int lane) {
+  for (; n >= 2; n -= 2) {
+    leaf_block_t4<CLS, 2, HYB>(st, pa, pb, acc0, acc1, sd);
+    st.advance(2, ops, bf, lane);
+  }
+  if (n) {
+    leaf_block_t4<CLS, 1, HYB>(st, pa, pb, acc0, acc1, sd);
+    st.advance(1, ops, bf, lane);
+  }
+}
+
+__device__ __forceinline__ uint32_t w4_nch(uint32_t w) { return w & 0x7FFu; }
+__device__ __forceinline__ uint32_t w4_nh(uint32_t w) { return (w >> 11) & 0x7FFu; }
+__device__ __forceinline__ uint32_t w4_ns(uint32_t w) { return w >> 22; }
+
+template <int D, int NU, bool HYB, typename BaseFn>
+__device__ __forceinline__ void k2t4_visit(Ring4& st, uint32_t w, double2 pa, double2 pb, double& acc0,
+                                           double& acc1, const SeedsT4<HYB>& sd, const int4* ops, BaseFn bf,
+                                           int lane) {
+  if constexpr (D > NU) {
+    return;
+  } else if constexpr (D == NU) {
+    const uint32_t n = w4_nch(w), nh = w4_nh(w), ns = w4_ns(w);
+    leaves_t4<0, HYB>(st, nh, pa, pb, acc0, acc1, sd, ops, bf, lane);
+    leaves_t4<1, HYB>(st, ns, pa, pb, acc0, acc1, sd, ops, bf, lane);
+    if (HYB) leaves_t4<2, HYB>(st, n - nh - ns, pa, pb, acc0, acc1, sd, ops, bf, lane);
+  } else {
+    const uint32_t n = w4_nch(w), nh = w4_nh(w), nhs = nh + w4_ns(w);
+    for (uint32_t j = 0; j < n; ++j) {
+      const int4 r = st.at(0);
+      st.advance(1, ops, bf, lane);
+      double2 sa, sb;
+      sd.get((uint32_t)r.z, j < nh ? 0u : (j < nhs ? 1u : 2u), sa, sb);
+      const double2 va = cmul(sa, pa), vb = cmul(sb, pb);
+      const double c = rec_c(r);
+      acc0 += c * va.x;
+      acc1 += c * vb.x;
+      k2t4_visit<D + 1, NU, HYB>(st, (uint32_t)r.w, va, vb, acc0, acc1, sd, ops, bf, lane);
+    }
+  }
+}
+
+template <int NU, int WARPS, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k2_tmem4(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
+         int Us_cold, const Op* __restrict__ ops4, const int32_t* __restrict__ chunk,
+         const int32_t* __restrict__ croots, int nchunk, double* __restrict__ out, double2* __restrict__ gcache,
+         double* __restrict__ part) {
+  unsigned char* smem = g_smem;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rows = U + 1;
+  const int hot = rows < (int)kTmemRows2 ? rows : (int)kTmemRows2;
+  const int cold = rows - hot;
+  const int us = cold < Us_cold ? cold : Us_cold;
+  double2* sC = reinterpret_cast<double2*>(smem);  // [us][64]
+  const uint32_t rings = (uint32_t)((size_t)us * 1024);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + rings + WARPS * Ring4::kAlloc);
+  double2* gC = HYB ? gcache + (size_t)blockIdx.x * (cold - us) * 64 : nullptr;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tbase = *tslot;
+  SeedsT4<HYB> sd;
+  sd.tq = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+  sd.sb = (uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)(lane * 16);
+  sd.gb = HYB ? reinterpret_cast<const char*>(gC) + lane * 16 : nullptr;
+  const int4* ops = reinterpret_cast<const int4*>(ops4);
+  auto ring_base = [=]() {
+    return (uint32_t)__cvta_generic_to_shared(g_smem) + rings + (uint32_t)((threadIdx.x >> 5) * Ring4::kAlloc);
+  };
+  double* mypart = part + (size_t)blockIdx.x * WARPS * 64;
+  Ring4 st;
   const int64_t ntiles = (S + 63) / 64;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t sa_i = tile * 64 + lane, sb_i = sa_i + 32;
@@ -959,19 +1262,20 @@ k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
     double wa = 0.0, wb = 0.0;
     for (int ci = warp; ci < nchunk; ci += WARPS) {
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
-      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), ring, lane);
-      while (st.i < st.n) {
+      const int32_t nr = __ldg(croots + ci);
+      st.begin(ops, (uint32_t)b, (uint32_t)e, ring_base(), lane);
+      for (int32_t k = 0; k < nr; ++k) {
         const int4 r0 = st.at(0), r1 = st.at(1);
-        st.advance(2, lane);
-        const uint32_t fl = (uint32_t)r1.w >> 16;
+        st.advance(2, ops, ring_base, lane);
+        const uint32_t fl = (uint32_t)r1.w;
         double2 a0, b0, a1, b1;
-        sd.get((uint32_t)r0.z, fl & 1u, a0, b0);
-        sd.get((uint32_t)r1.z, (fl >> 1) & 1u, a1, b1);
+        sd.get((uint32_t)r0.z, fl & 3u, a0, b0);
+        sd.get((uint32_t)r1.z, (fl >> 2) & 3u, a1, b1);
         const double2 va = cmul(a0, a1), vb = cmul(b0, b1);
         const double c = rec_c(r0);
         wa += c * va.x;
         wb += c * vb.x;
-        k2t3_visit<3, NU, HYB>(st, rec_nch(r0), (uint32_t)r0.w >> 16, va, vb, wa, wb, sd, lane);
+        k2t4_visit<3, NU, HYB>(st, (uint32_t)r0.w, va, vb, wa, wb, sd, ops, ring_base, lane);
       }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -990,6 +1294,261 @@ k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
+// ------------------------------------- K2 (four sites per lane, TMEM + smem)
+// 128-site tiles: lane l handles sites l, l+32, l+64, l+96 of the tile, so
+// every program record (its load, decode, seed addressing and loop control)
+// serves four sites -- the per-record overhead that bounds k2_tmem2/3 is
+// amortised twice as far.  Seed rows are 2 KB ([4][32] c128): the 32 hottest
+// in TMEM (16 columns per lane, one x16 load per fetch, replicated per lane
+// quadrant), the next in shared memory, the tail in the per-CTA global
+// cache.  16 warps x 128 registers.
+constexpr uint32_t kTmemRowsQ = 32;
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+}
+
+struct C4 {
+  double2 v[4];
+};
+
+template <bool HYB>
+struct SeedsQ {
+  uint32_t tq;      // TMEM address of this warp's quadrant, column 0
+  uint32_t sb;      // shared address of cold row 0 + lane * 16
+  const char* gb;   // global cache of this CTA + lane * 16
+  uint32_t usB;     // shared-memory cold rows * 2048
+  // records carry slot * 512: hot slot s -> TMEM column 16 s; cold -> 2 KB row
+  __device__ __forceinline__ void hot_issue(uint32_t off, uint32_t (&t)[16]) const { tmem_ld16(tq + (off >> 5), t); }
+  __device__ __forceinline__ static C4 unpack(const uint32_t (&t)[16]) {
+    C4 s;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      s.v[k] = make_double2(__hiloint2double(t[4 * k + 1], t[4 * k]), __hiloint2double(t[4 * k + 3], t[4 * k + 2]));
+    return s;
+  }
+  __device__ __forceinline__ C4 cold(uint32_t off) const {
+    const uint32_t c = off * 4 - kTmemRowsQ * 2048;  // byte offset of the 2 KB cold row
+    C4 s;
+    if (!HYB || c < usB) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(s.v[k].x), "=d"(s.v[k].y) : "r"(sb + c + k * 512));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s.v[k] = *reinterpret_cast<const double2*>(gb + (c - usB) + k * 512);
+    }
+    return s;
+  }
+  __device__ __forceinline__ C4 get(uint32_t off, bool hot) const {
+    if (hot) {
+      uint32_t t[16];
+      hot_issue(off, t);
+      tmem_wait_ld();
+      return unpack(t);
+    }
+    return cold(off);
+  }
+};
+
+__device__ __forceinline__ C4 cmul4(const C4& a, const C4& b) {
+  C4 r;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) r.v[k] = cmul(a.v[k], b.v[k]);
+  return r;
+}
+
+template <bool HOT, int K, bool HYB>
+__device__ __forceinline__ void leaf_block_q(const Ring3& st, const C4& pv, double (&acc)[4], const SeedsQ<HYB>& sd) {
+  int4 r[K];
+  C4 s[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = st.at(j);
+  if constexpr (HOT) {
+    uint32_t t[K][16];
+#pragma unroll
+    for (int j = 0; j < K; ++j) sd.hot_issue((uint32_t)r[j].z, t[j]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < K; ++j) s[j] = SeedsQ<HYB>::unpack(t[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) s[j] = sd.cold((uint32_t)r[j].z);
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const double c = rec_c(r[j]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] = __fma_rn(c, re_mul(s[j].v[k], pv.v[k]), acc[k]);
+  }
+}
+
+template <bool HOT, int MAXU, bool HYB>
+__device__ __forceinline__ void leaves_q(Ring3& st, uint32_t n, const C4& pv, double (&acc)[4], const SeedsQ<HYB>& sd,
+                                         int lane) {
+  if constexpr (MAXU >= 2) {
+    for (; n >= 2; n -= 2) {
+      leaf_block_q<HOT, 2, HYB>(st, pv, acc, sd);
+      st.advance(2, lane);
+    }
+  }
+  for (; n; --n) {
+    leaf_block_q<HOT, 1, HYB>(st, pv, acc, sd);
+    st.advance(1, lane);
+  }
+}
+
+template <int D, int NU, int MAXU, bool HYB>
+__device__ __forceinline__ void k2q_visit(Ring3& st, uint32_t n, uint32_t nh, const C4& pv, double (&acc)[4],
+                                          const SeedsQ<HYB>& sd, int lane) {
+  if constexpr (D > NU) {
+    return;
+  } else if constexpr (D == NU) {
+    leaves_q<true, MAXU, HYB>(st, nh, pv, acc, sd, lane);
+    leaves_q<false, MAXU, HYB>(st, n - nh, pv, acc, sd, lane);
+  } else {
+    for (uint32_t j = 0; j < n; ++j) {
+      const int4 r = st.at(0);
+      st.advance(1, lane);
+      const C4 v = cmul4(sd.get((uint32_t)r.z, j < nh), pv);
+      const double c = rec_c(r);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = __fma_rn(c, v.v[k].x, acc[k]);
+      k2q_visit<D + 1, NU, MAXU, HYB>(st, rec_nch(r), (uint32_t)r.w >> 16, v, acc, sd, lane);
+    }
+  }
+}
+
+template <int NU, int WARPS, int MAXU, bool HYB>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
+        int Us_cold, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
+        double* __restrict__ out, double2* __restrict__ gcache, double* __restrict__ part, int64_t full_tiles,
+        int tail_parts, double* __restrict__ tailbuf) {
+  unsigned char* smem = g_smem;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rows = U + 1;
+  const int hot = rows < (int)kTmemRowsQ ? rows : (int)kTmemRowsQ;
+  const int cold = rows - hot;
+  const int us = cold < Us_cold ? cold : Us_cold;
+  double2* sC = reinterpret_cast<double2*>(smem);  // [us][128]
+  const uint32_t rings = (uint32_t)((size_t)us * 2048);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + rings + WARPS * Ring3::kAlloc);
+  double2* gC = HYB ? gcache + (size_t)blockIdx.x * (cold - us) * 128 : nullptr;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tbase = *tslot;
+  SeedsQ<HYB> sd;
+  sd.tq = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+  sd.sb = (uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)(lane * 16);
+  sd.gb = HYB ? reinterpret_cast<const char*>(gC) + lane * 16 : nullptr;
+  sd.usB = (uint32_t)us * 2048u;
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem + rings + warp * Ring3::kAlloc);
+  double* mypart = part + (size_t)blockIdx.x * nchunk * 128;
+  Ring3 st;
+  // work items: whole tiles, then the last partial round's tiles split into
+  // tail_parts program slices each (partial sums to tailbuf, summed in slice
+  // order by k_tail_reduce) so the final round still fills the grid
+  const int64_t ntiles = (S + 127) / 128;
+  const int64_t nitems = full_tiles + (ntiles - full_tiles) * tail_parts;
+  for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const bool whole = it < full_tiles;
+    const int64_t tile = whole ? it : full_tiles + (it - full_tiles) / tail_parts;
+    const int slice = whole ? 0 : (int)((it - full_tiles) % tail_parts);
+    const int nsl = whole ? 1 : tail_parts;
+    const int cb = (int)((int64_t)slice * nchunk / nsl), ce = (int)((int64_t)(slice + 1) * nchunk / nsl);
+    const double2* row[4];
+    bool ok[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t s = tile * 128 + k * 32 + lane;
+      ok[k] = s < S;
+      row[k] = A + (ok[k] ? s : 0) * (int64_t)L;
+    }
+    for (int h = warp >> 2; h < hot; h += WARPS / 4) {
+      double2 v[4];
+      const int lab = h == U ? 0 : __ldg(slot_label + h);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        v[k] = h == U ? make_double2(1.0, 0.0) : (ok[k] ? ld_stream(row[k] + lab) : make_double2(0.0, 0.0));
+      tmem_st8(sd.tq + (uint32_t)h * 16, v[0], v[1]);
+      tmem_st8(sd.tq + (uint32_t)h * 16 + 8, v[2], v[3]);
+    }
+    for (int c = warp; c < cold; c += WARPS) {
+      const int u = hot + c;
+      const int lab = u == U ? 0 : __ldg(slot_label + u);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double2 v =
+            u == U ? make_double2(1.0, 0.0) : (ok[k] ? ld_stream(row[k] + lab) : make_double2(0.0, 0.0));
+        if (!HYB || c < us) sC[c * 128 + k * 32 + lane] = v;
+        else gC[(size_t)(c - us) * 128 + k * 32 + lane] = v;
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    // one partial per (chunk, site), summed in chunk order (as k2_tmem3)
+    double* dst = whole ? mypart : tailbuf + (size_t)((it - full_tiles) / tail_parts) * nchunk * 128;
+    for (int ci = cb + warp; ci < ce; ci += WARPS) {
+      const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
+      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), ring, lane);
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      while (st.i < st.n) {
+        const int4 r0 = st.at(0), r1 = st.at(1);
+        st.advance(2, lane);
+        const uint32_t fl = (uint32_t)r1.w >> 16;
+        const C4 v = cmul4(sd.get((uint32_t)r0.z, fl & 1u), sd.get((uint32_t)r1.z, (fl >> 1) & 1u));
+        const double c = rec_c(r0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = __fma_rn(c, v.v[k].x, acc[k]);
+        k2q_visit<3, NU, MAXU, HYB>(st, rec_nch(r0), (uint32_t)r0.w >> 16, v, acc, sd, lane);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[(size_t)ci * 128 + k * 32 + lane] = acc[k];
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (whole && threadIdx.x < 128) {
+      double s = 0.0;
+#pragma unroll 16
+      for (int ci = 0; ci < nchunk; ++ci) s += __ldcg(mypart + (size_t)ci * 128 + threadIdx.x);
+      const int64_t site = tile * 128 + threadIdx.x;
+      if (site < S) out[site] = s;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
+// tail tiles: out[site] = sum over chunks (in chunk order) of the partials
+__global__ void k_tail_reduce(const double* __restrict__ tailbuf, int64_t first_site, int64_t S, int tile_sites,
+                              int nchunk, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // site offset past first_site
+  if (first_site + i >= S) return;
+  const int64_t t = i / tile_sites, o = i % tile_sites;
+  const double* p = tailbuf + t * nchunk * tile_sites + o;
+  double s = 0.0;
+#pragma unroll 16
+  for (int c = 0; c < nchunk; ++c) s += p[(size_t)c * tile_sites];
+  out[first_site + i] = s;
 }
 
 // ------------------------------------------------------ K2 (two sites/lane)

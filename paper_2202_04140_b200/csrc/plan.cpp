@@ -168,13 +168,13 @@ void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re, c
   std::vector<int32_t> roots = singles;
   roots.insert(roots.end(), by_order[2].begin(), by_order[2].end());
   std::sort(roots.begin(), roots.end(), by_tuple);
-  // children whose seed is TMEM-resident (slot < hot_rows) first
+  // children by seed slot: the TMEM-resident seeds (slot < hot_rows) lead,
+  // then the shared-memory rows, then the global-cache tail (distinct
+  // children of one node have distinct seeds, so the order is total)
   auto hot = [&](int32_t k) { return slot[nodes[k].sec] < hot_rows; };
   for (auto& n : nodes)
-    std::sort(n.kids.begin(), n.kids.end(), [&](int32_t a, int32_t b) {
-      if (hot(a) != hot(b)) return hot(a);
-      return nodes[a].t < nodes[b].t;
-    });
+    std::sort(n.kids.begin(), n.kids.end(),
+              [&](int32_t a, int32_t b) { return slot[nodes[a].sec] < slot[nodes[b].sec]; });
   P.max_order = std::max(2, max_order);
 
   // Records (16 B): {c, byte offset of the seed row, #children, subtree size}.

@@ -162,12 +162,14 @@ class SitePlan:
         self.complex_coef = cplx
         return self
 
-    def kernel_name(self, method: str = "recursive", prec: str = "f64", out: str = "real") -> str:
-        """The kernel evaluate() launches for these arguments (reporting)."""
+    def kernel_name(self, method: str = "recursive", prec: str = "f64", out: str = "real",
+                    sites: int = 1 << 20) -> str:
+        """The kernel evaluate() launches for these arguments on ``sites``
+        sites (reporting)."""
         return N.lib().acedag_eval_kernel_name(
             self._h, N.METHOD_NAIVE if method == "naive" else N.METHOD_RECURSIVE,
-            N.PREC_F32 if prec == "f32" else N.PREC_F64, N.OUT_COMPLEX if out == "complex" else N.OUT_REAL
-        ).decode()
+            N.PREC_F32 if prec == "f32" else N.PREC_F64, N.OUT_COMPLEX if out == "complex" else N.OUT_REAL,
+            int(sites)).decode()
 
     def info(self) -> dict:
         a, b, c, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()

@@ -259,6 +259,20 @@ def test_host_pipelines_match_device(cuda, cfg2, golden):
                        plan.evaluate_positions_host(xyz.pin_memory(), chunk=2).clone())
 
 
+def test_batch_independent_results(cuda, cfg2):
+    """A site's phi does not depend on the batch it is evaluated in: the
+    default kernels sum one partial per program chunk in chunk order, so the
+    tile geometry (k2_quad / k2_tmem3), the last-round split and the site
+    count leave every value bit-identical."""
+    c = np.random.default_rng(34).normal(size=len(cfg2.target_ids))
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
+    A = torch.from_numpy(seeded_A(40_000, cfg2.num_seeds, 35)).to(cuda)
+    full = plan.evaluate(A)
+    for n in (1, 63, 64, 1000, 9_500, 19_000, 30_001):
+        assert torch.equal(plan.evaluate(A[:n]), full[:n]), n
+    assert torch.equal(plan.evaluate(A[7_000:27_000]), full[7_000:27_000])
+
+
 def test_eval_host_variants(cuda, cfg2):
     """acedag_eval_host for the naive method, fp32 mode, several outputs and
     complex output agrees bit for bit with acedag_eval on the device."""
@@ -280,7 +294,7 @@ def test_eval_host_variants(cuda, cfg2):
     assert plan3.evaluate_host(Ap[:0]).shape == (0, 3)
 
 
-@pytest.mark.parametrize("env", [{"ACEDAG_K2_SPL": "1"}, {"ACEDAG_K2_SPL": "1", "ACEDAG_K2_WARPS": "16"},
+@pytest.mark.parametrize("env", [{"ACEDAG_K2_SPL": "1"}, {"ACEDAG_K2": "tmem2"}, {"ACEDAG_K2_SPL": "1", "ACEDAG_K2_WARPS": "16"},
                                  {"ACEDAG_SCHED": "1"}, {"ACEDAG_MULTI": "scalar"}])
 def test_kernel_variants_in_subprocess(cuda, env):
     """The alternative K2 geometries (32-site tiles, 16 warps, dynamic chunk

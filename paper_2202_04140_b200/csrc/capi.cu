@@ -917,7 +917,8 @@ int quad_launch(acedag_plan* P, int64_t S, Launch& lc) {
   lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
   lc.rows = P->U + 1;
   const int cold = std::max(0, lc.rows - (int)dev::kTmemRowsQ);
-  const size_t fixed = (size_t)16 * dev::Ring3::kAlloc + 16;
+  // rings, TMEM slot + chunk counter (16 B), slot -> label table
+  const size_t fixed = (size_t)16 * dev::Ring3::kAlloc + 16 + (((size_t)lc.rows * 4 + 15) & ~(size_t)15);
   const int us_max = (int)((P->smem_optin - fixed) / 2048);
   lc.us = std::min(cold, us_max);
   lc.hyb = lc.us < cold;

@@ -1441,6 +1441,9 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
   double2* sC = reinterpret_cast<double2*>(smem);  // [us][128]
   const uint32_t rings = (uint32_t)((size_t)us * 2048);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + rings + WARPS * Ring3::kAlloc);
+  int* dyn = reinterpret_cast<int*>(tslot) + 1;        // next chunk of the current item
+  int32_t* slab = reinterpret_cast<int32_t*>(tslot) + 4;  // slot -> label (-1: the ONE row)
+  for (int h = threadIdx.x; h < rows; h += blockDim.x) slab[h] = h == U ? -1 : (int32_t)__ldg(slot_label + h);
   double2* gC = HYB ? gcache + (size_t)blockIdx.x * (cold - us) * 128 : nullptr;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
@@ -1478,33 +1481,58 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
       ok[k] = s < S;
       row[k] = A + (ok[k] ? s : 0) * (int64_t)L;
     }
-    for (int h = warp >> 2; h < hot; h += WARPS / 4) {
-      double2 v[4];
-      const int lab = h == U ? 0 : __ldg(slot_label + h);
+    // staging: four rows per pass, sixteen loads in flight per lane
+    for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (WARPS / 4)) {
+      double2 v[4][4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        v[k] = h == U ? make_double2(1.0, 0.0) : (ok[k] ? ld_stream(row[k] + lab) : make_double2(0.0, 0.0));
-      tmem_st8(sd.tq + (uint32_t)h * 16, v[0], v[1]);
-      tmem_st8(sd.tq + (uint32_t)h * 16 + 8, v[2], v[3]);
-    }
-    for (int c = warp; c < cold; c += WARPS) {
-      const int u = hot + c;
-      const int lab = u == U ? 0 : __ldg(slot_label + u);
+      for (int q = 0; q < 4; ++q) {
+        const int h = h0 + q * (WARPS / 4);
+        const int lab = h < hot ? slab[h] : -1;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double2 v =
-            u == U ? make_double2(1.0, 0.0) : (ok[k] ? ld_stream(row[k] + lab) : make_double2(0.0, 0.0));
-        if (!HYB || c < us) sC[c * 128 + k * 32 + lane] = v;
-        else gC[(size_t)(c - us) * 128 + k * 32 + lane] = v;
+        for (int k = 0; k < 4; ++k)
+          v[q][k] = (lab >= 0 && ok[k]) ? ld_stream(row[k] + lab) : make_double2(h == U ? 1.0 : 0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int h = h0 + q * (WARPS / 4);
+        if (h < hot) {
+          tmem_st8(sd.tq + (uint32_t)h * 16, v[q][0], v[q][1]);
+          tmem_st8(sd.tq + (uint32_t)h * 16 + 8, v[q][2], v[q][3]);
+        }
       }
     }
+    for (int c0 = warp; c0 < cold; c0 += 4 * WARPS) {
+      double2 v[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + q * WARPS;
+        const int lab = c < cold ? slab[hot + c] : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          v[q][k] = (lab >= 0 && ok[k]) ? ld_stream(row[k] + lab) : make_double2(hot + c == U ? 1.0 : 0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + q * WARPS;
+        if (c < cold) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (!HYB || c < us) sC[c * 128 + k * 32 + lane] = v[q][k];
+            else gC[(size_t)(c - us) * 128 + k * 32 + lane] = v[q][k];
+          }
+        }
+      }
+    }
+    if (threadIdx.x == 0) *dyn = cb + WARPS;
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     // one partial per (chunk, site), summed in chunk order (as k2_tmem3)
     double* dst = whole ? mypart : tailbuf + (size_t)((it - full_tiles) / tail_parts) * nchunk * 128;
-    for (int ci = cb + warp; ci < ce; ci += WARPS) {
+    // chunks handed out dynamically (the partials are indexed by chunk, so
+    // the result does not depend on which warp ran which chunk)
+    for (int ci = cb + warp; ci < ce;) {
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
       st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), ring, lane);
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1520,6 +1548,9 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) dst[(size_t)ci * 128 + k * 32 + lane] = acc[k];
+      int nx = 0;
+      if (lane == 0) nx = atomicAdd(dyn, 1);
+      ci = __shfl_sync(0xffffffffu, nx, 0);
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n");

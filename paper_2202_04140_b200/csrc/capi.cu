@@ -285,6 +285,7 @@ struct acedag_plan {
   // each slot's column in it
   DevBuf<int32_t> sorted_labels;
   DevBuf<uint16_t> slot_sorted;
+  DevBuf<uint16_t> sorted_slot;  // inverse: sorted position -> slot
   DevBuf<int32_t> col_of;  // label -> seed slot or -1 (pool of used labels only)
   DevBuf<int4> tri;        // (n, l, m >= 0) triples the used labels need
   DevBuf<Op> ops;
@@ -301,6 +302,7 @@ struct acedag_plan {
   // distinct streams may run concurrently
   struct Workspace {
     DevBuf<double> tail;  // split last-round partials
+    DevBuf<double2> tiles;  // tile-major seed table (k_tile_seeds)
     DevBuf<double2> gcache;
     DevBuf<double2> ws_A;
     DevBuf<double> part;  // K2 partial sums
@@ -521,6 +523,9 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
       pos[i] = (uint16_t)(std::lower_bound(sorted.begin(), sorted.end(), used[i]) - sorted.begin());
     CK(P->sorted_labels.upload(sorted));
     CK(P->slot_sorted.upload(pos));
+    std::vector<uint16_t> inv(P->U);
+    for (int i = 0; i < P->U; ++i) inv[pos[i]] = (uint16_t)i;
+    CK(P->sorted_slot.upload(inv));
   }
   {
     std::vector<int32_t> col((size_t)P->g->n_seeds(), -1);
@@ -877,12 +882,34 @@ cudaError_t launch_tmem4_k(acedag_plan* P, const double2* A, int64_t S, int L, c
   return cudaGetLastError();
 }
 
+// ACEDAG_TILED=0 stages k2_quad's seeds straight from A (no tile-major copy)
+bool use_tiled() {
+  static bool v = [] {
+    const char* e = getenv("ACEDAG_TILED");
+    return !(e && std::string(e) == "0");
+  }();
+  return v;
+}
+
 template <int NU, bool HYB>
 cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
                           double* out, const Launch& lc, cudaStream_t st) {
   constexpr int W = 16;
   const bool two = getenv("ACEDAG_K2_MAXU") ? k2_maxu() >= 2 : NU <= 4;
-  auto k = two ? dev::k2_quad<NU, W, 2, HYB> : dev::k2_quad<NU, W, 1, HYB>;
+  // tile-major copy of the used seeds: which columns of A feed which rows
+  const int32_t* cols = nullptr;
+  const uint16_t* slots = nullptr;
+  bool tiled = use_tiled();
+  if (slot_label == P->slot_label.p) {
+    cols = P->sorted_labels.p;
+    slots = P->sorted_slot.p;
+  } else if (slot_label == P->slot_sorted.p) {
+    slots = P->sorted_slot.p;
+  } else if (slot_label != P->slot_identity.p) {
+    tiled = false;
+  }
+  auto k = tiled ? (two ? dev::k2_quad<NU, W, 2, HYB, true> : dev::k2_quad<NU, W, 1, HYB, true>)
+                 : (two ? dev::k2_quad<NU, W, 2, HYB, false> : dev::k2_quad<NU, W, 1, HYB, false>);
   cudaError_t e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
   e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 128);
@@ -895,7 +922,23 @@ cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, co
     e = lc.ws->tail.alloc((size_t)(ntiles - full) * nchunks(P) * 128);
     if (e != cudaSuccess) return e;
   }
-  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->opsQ.p, P->chunk.p, nchunks(P),
+  const double2* src = A;
+  if (tiled) {
+    e = lc.ws->tiles.alloc((size_t)ntiles * (P->U + 1) * 128);
+    if (e != cudaSuccess) return e;
+    constexpr size_t tsm = 32 * 129 * 16;
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(dev::k_tile_seeds<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dev::k_tile_seeds<128><<<(unsigned)ntiles, 512, tsm, st>>>(A, S, L, cols, slots, P->U, lc.ws->tiles.p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    src = lc.ws->tiles.p;
+  }
+  k<<<lc.grid, lc.block, lc.smem, st>>>(src, S, L, slot_label, P->U, lc.us, P->opsQ.p, P->chunk.p, nchunks(P),
                                         out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p);
   e = cudaGetLastError();
   if (e != cudaSuccess || parts == 1) return e;

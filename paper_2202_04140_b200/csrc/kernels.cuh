@@ -1296,6 +1296,46 @@ k2_tmem4(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
 }
 
+// --------------------------------------------- tile-major seed table (K2 input)
+// A [S, L] c128 -> T [ntiles][U + 1][TS] c128: row r of tile t holds slot r
+// (row U = the constant ONE) for the TS sites of the tile, so the K2 kernels
+// stage and fetch whole rows with coalesced loads.  Lanes walk the used
+// columns in ascending order (coalesced reads of each site row); a padded
+// [32][TS + 1] shared block transposes 32 columns at a time.
+// cols: column of the j-th used entry (NULL: j); slots: its row (NULL: j).
+template <int TS>
+__global__ void __launch_bounds__(512) k_tile_seeds(const double2* __restrict__ A, int64_t S, int L,
+                                                    const int32_t* __restrict__ cols,
+                                                    const uint16_t* __restrict__ slots, int U,
+                                                    double2* __restrict__ T) {
+  extern __shared__ double2 tb[];  // [32][TS + 1]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = 16;
+  const int64_t tile = blockIdx.x;
+  const int R = U + 1;
+  double2* Tt = T + tile * (int64_t)R * TS;
+  for (int j0 = 0; j0 < U; j0 += 32) {
+    const int j = j0 + lane;
+    const int col = j < U ? (cols ? __ldg(cols + j) : j) : -1;
+    double2 v[TS / NW];
+#pragma unroll
+    for (int q = 0; q < TS / NW; ++q) {
+      const int64_t site = tile * TS + warp + q * NW;
+      v[q] = (col >= 0 && site < S) ? ld_stream(A + site * L + col) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < TS / NW; ++q) tb[lane * (TS + 1) + warp + q * NW] = v[q];
+    __syncthreads();
+    for (int jj = warp; jj < 32 && j0 + jj < U; jj += NW) {
+      const int slot = slots ? (int)__ldg(slots + j0 + jj) : j0 + jj;
+#pragma unroll
+      for (int q = 0; q < TS / 32; ++q) Tt[(int64_t)slot * TS + q * 32 + lane] = tb[jj * (TS + 1) + q * 32 + lane];
+    }
+    __syncthreads();
+  }
+  for (int q = threadIdx.x; q < TS; q += blockDim.x) Tt[(int64_t)U * TS + q] = make_double2(1.0, 0.0);
+}
+
 // ------------------------------------- K2 (four sites per lane, TMEM + smem)
 // 128-site tiles: lane l handles sites l, l+32, l+64, l+96 of the tile, so
 // every program record (its load, decode, seed addressing and loop control)
@@ -1426,7 +1466,9 @@ __device__ __forceinline__ void k2q_visit(Ring3& st, uint32_t n, uint32_t nh, co
   }
 }
 
-template <int NU, int WARPS, int MAXU, bool HYB>
+// TILED: A is the tile-major table of k_tile_seeds (rows staged with
+// coalesced loads; the global-cache tail is read from it in place)
+template <int NU, int WARPS, int MAXU, bool HYB, bool TILED>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
         int Us_cold, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
@@ -1444,7 +1486,7 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
   int* dyn = reinterpret_cast<int*>(tslot) + 1;        // next chunk of the current item
   int32_t* slab = reinterpret_cast<int32_t*>(tslot) + 4;  // slot -> label (-1: the ONE row)
   for (int h = threadIdx.x; h < rows; h += blockDim.x) slab[h] = h == U ? -1 : (int32_t)__ldg(slot_label + h);
-  double2* gC = HYB ? gcache + (size_t)blockIdx.x * (cold - us) * 128 : nullptr;
+  double2* gC = (HYB && !TILED) ? gcache + (size_t)blockIdx.x * (cold - us) * 128 : nullptr;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
         (uint32_t)__cvta_generic_to_shared(tslot)));
@@ -1481,6 +1523,36 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
       ok[k] = s < S;
       row[k] = A + (ok[k] ? s : 0) * (int64_t)L;
     }
+    const double2* Tt = A + tile * (int64_t)rows * 128;  // TILED: this tile's rows
+    if (TILED && HYB) sd.gb = reinterpret_cast<const char*>(Tt + (size_t)(hot + us) * 128) + lane * 16;
+    if constexpr (TILED) {
+      for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (WARPS / 4)) {
+        double2 v[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int h = h0 + q * (WARPS / 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[q][k] = h < hot ? ld_stream(Tt + (size_t)h * 128 + k * 32 + lane) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int h = h0 + q * (WARPS / 4);
+          if (h < hot) {
+            tmem_st8(sd.tq + (uint32_t)h * 16, v[q][0], v[q][1]);
+            tmem_st8(sd.tq + (uint32_t)h * 16 + 8, v[q][2], v[q][3]);
+          }
+        }
+      }
+      // shared-memory rows: asynchronous 16-byte copies, no registers
+      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sC);
+      for (int idx = threadIdx.x; idx < us * 128; idx += WARPS * 32) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + idx * 16),
+                     "l"(Tt + (size_t)hot * 128 + idx)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    } else {
     // staging: four rows per pass, sixteen loads in flight per lane
     for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (WARPS / 4)) {
       double2 v[4][4];
@@ -1522,6 +1594,7 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
           }
         }
       }
+    }
     }
     if (threadIdx.x == 0) *dyn = cb + WARPS;
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");

@@ -823,12 +823,50 @@ void tail_split(int64_t ntiles, int grid, int nchunk, int64_t& full, int& parts)
   parts = p;
 }
 
+int tiled_mode();
+bool use_tiled();
+
+// the tile-major seed copy (k_tile_seeds<TS>) for an eval_impl input, or
+// false when the input layout is not one the plan knows
+template <int TS>
+bool tile_seeds(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+                acedag_plan::Workspace* ws, cudaStream_t st, cudaError_t& e) {
+  e = cudaSuccess;
+  const int32_t* cols = nullptr;
+  const uint16_t* slots = nullptr;
+  if (slot_label == P->slot_label.p) {
+    cols = P->sorted_labels.p;
+    slots = P->sorted_slot.p;
+  } else if (slot_label == P->slot_sorted.p) {
+    slots = P->sorted_slot.p;
+  } else if (slot_label != P->slot_identity.p) {
+    return false;
+  }
+  const int64_t ntiles = (S + TS - 1) / TS;
+  e = ws->tiles.alloc((size_t)ntiles * (P->U + 1) * TS);
+  if (e != cudaSuccess) return true;
+  constexpr size_t tsm = 32 * (TS + 1) * 16;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(dev::k_tile_seeds<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    if (e != cudaSuccess) return true;
+    attr = true;
+  }
+  dev::k_tile_seeds<TS><<<(unsigned)ntiles, 512, tsm, st>>>(A, S, L, cols, slots, P->U, ws->tiles.p);
+  e = cudaGetLastError();
+  return true;
+}
+
 template <int NU, bool HYB>
 cudaError_t launch_tmem3_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
                            double* out, const Launch& lc, cudaStream_t st) {
   constexpr int W = 32;
-  auto k = dev::k2_tmem3<NU, W, HYB>;
-  cudaError_t e = set_smem(k, lc.smem);
+  cudaError_t e;
+  const bool tiled = tiled_mode() >= 2 && tile_seeds<64>(P, A, S, L, slot_label, lc.ws, st, e);
+  if (tiled && e != cudaSuccess) return e;
+  if (tiled) A = lc.ws->tiles.p;
+  auto k = tiled ? dev::k2_tmem3<NU, W, HYB, true> : dev::k2_tmem3<NU, W, HYB, false>;
+  e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
   e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 64);
   if (e != cudaSuccess) return e;
@@ -882,35 +920,30 @@ cudaError_t launch_tmem4_k(acedag_plan* P, const double2* A, int64_t S, int L, c
   return cudaGetLastError();
 }
 
-// ACEDAG_TILED=0 stages k2_quad's seeds straight from A (no tile-major copy)
-bool use_tiled() {
-  static bool v = [] {
+// tile-major seed copy: ACEDAG_TILED=0 never, 1 (default) for k2_quad,
+// 2 also for k2_tmem3 (measured slower there: cfg4's long global tail is
+// better served by the per-CTA cache that stays in L2; cfg1 is launch-bound)
+int tiled_mode() {
+  static int v = [] {
     const char* e = getenv("ACEDAG_TILED");
-    return !(e && std::string(e) == "0");
+    return e ? atoi(e) : 1;
   }();
   return v;
 }
+bool use_tiled() { return tiled_mode() >= 1; }
 
 template <int NU, bool HYB>
 cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
                           double* out, const Launch& lc, cudaStream_t st) {
   constexpr int W = 16;
   const bool two = getenv("ACEDAG_K2_MAXU") ? k2_maxu() >= 2 : NU <= 4;
-  // tile-major copy of the used seeds: which columns of A feed which rows
-  const int32_t* cols = nullptr;
-  const uint16_t* slots = nullptr;
-  bool tiled = use_tiled();
-  if (slot_label == P->slot_label.p) {
-    cols = P->sorted_labels.p;
-    slots = P->sorted_slot.p;
-  } else if (slot_label == P->slot_sorted.p) {
-    slots = P->sorted_slot.p;
-  } else if (slot_label != P->slot_identity.p) {
-    tiled = false;
-  }
+  cudaError_t e;
+  const bool tiled = use_tiled() && tile_seeds<128>(P, A, S, L, slot_label, lc.ws, st, e);
+  if (tiled && e != cudaSuccess) return e;
+  if (tiled) A = lc.ws->tiles.p;
   auto k = tiled ? (two ? dev::k2_quad<NU, W, 2, HYB, true> : dev::k2_quad<NU, W, 1, HYB, true>)
                  : (two ? dev::k2_quad<NU, W, 2, HYB, false> : dev::k2_quad<NU, W, 1, HYB, false>);
-  cudaError_t e = set_smem(k, lc.smem);
+  e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
   e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 128);
   if (e != cudaSuccess) return e;
@@ -922,23 +955,7 @@ cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, co
     e = lc.ws->tail.alloc((size_t)(ntiles - full) * nchunks(P) * 128);
     if (e != cudaSuccess) return e;
   }
-  const double2* src = A;
-  if (tiled) {
-    e = lc.ws->tiles.alloc((size_t)ntiles * (P->U + 1) * 128);
-    if (e != cudaSuccess) return e;
-    constexpr size_t tsm = 32 * 129 * 16;
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(dev::k_tile_seeds<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    dev::k_tile_seeds<128><<<(unsigned)ntiles, 512, tsm, st>>>(A, S, L, cols, slots, P->U, lc.ws->tiles.p);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    src = lc.ws->tiles.p;
-  }
-  k<<<lc.grid, lc.block, lc.smem, st>>>(src, S, L, slot_label, P->U, lc.us, P->opsQ.p, P->chunk.p, nchunks(P),
+  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->opsQ.p, P->chunk.p, nchunks(P),
                                         out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p);
   e = cudaGetLastError();
   if (e != cudaSuccess || parts == 1) return e;

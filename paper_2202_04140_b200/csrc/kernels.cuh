@@ -889,7 +889,8 @@ __device__ __forceinline__ void k2t3_visit(Ring3& st, uint32_t n, uint32_t nh, d
   }
 }
 
-template <int NU, int WARPS, bool HYB>
+// TILED: A is the tile-major table of k_tile_seeds<64> (as k2_quad)
+template <int NU, int WARPS, bool HYB, bool TILED>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restrict__ slot_label, int U,
          int Us_cold, const Op* __restrict__ ops, const int32_t* __restrict__ chunk, int nchunk,
@@ -904,7 +905,7 @@ k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
   double2* sC = reinterpret_cast<double2*>(smem);  // [us][64]
   const uint32_t rings = (uint32_t)((size_t)us * 1024);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + rings + WARPS * Ring3::kAlloc);
-  double2* gC = HYB ? gcache + (size_t)blockIdx.x * (cold - us) * 64 : nullptr;
+  double2* gC = (HYB && !TILED) ? gcache + (size_t)blockIdx.x * (cold - us) * 64 : nullptr;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
         (uint32_t)__cvta_generic_to_shared(tslot)));
@@ -935,6 +936,32 @@ k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
     const bool va_ok = sa_i < S, vb_ok = sb_i < S;
     const double2* rowa = A + (va_ok ? sa_i : 0) * (int64_t)L;
     const double2* rowb = A + (vb_ok ? sb_i : 0) * (int64_t)L;
+    if constexpr (TILED) {
+      const double2* Tt = A + tile * (int64_t)rows * 64;
+      if (HYB) sd.g = reinterpret_cast<const char*>(Tt + (size_t)(hot + us) * 64) + lane * 16;
+      for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (WARPS / 4)) {
+        double2 v[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int h = h0 + q * (WARPS / 4);
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            v[q][k] = h < hot ? ld_stream(Tt + (size_t)h * 64 + k * 32 + lane) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int h = h0 + q * (WARPS / 4);
+          if (h < hot) tmem_st8(sd.tq + (uint32_t)h * 8, v[q][0], v[q][1]);
+        }
+      }
+      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sC);
+      for (int idx = threadIdx.x; idx < us * 64; idx += WARPS * 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + idx * 16),
+                     "l"(Tt + (size_t)hot * 64 + idx)
+                     : "memory");
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    } else {
     for (int h = warp >> 2; h < hot; h += WARPS / 4) {
       double2 a, b;
       if (h == U) {
@@ -963,6 +990,7 @@ k2_tmem3(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
         gC[(size_t)(c - us) * 64 + lane] = a;
         gC[(size_t)(c - us) * 64 + 32 + lane] = b;
       }
+    }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n");

@@ -295,11 +295,14 @@ def test_eval_host_variants(cuda, cfg2):
 
 
 @pytest.mark.parametrize("env", [{"ACEDAG_K2_SPL": "1"}, {"ACEDAG_K2": "tmem2"}, {"ACEDAG_K2_SPL": "1", "ACEDAG_K2_WARPS": "16"},
-                                 {"ACEDAG_SCHED": "1"}, {"ACEDAG_MULTI": "scalar"}])
+                                 {"ACEDAG_SCHED": "1"}, {"ACEDAG_MULTI": "scalar"}, {"ACEDAG_K2": "quad"},
+                                 {"ACEDAG_K2": "quad", "ACEDAG_TILED": "0"}, {"ACEDAG_TILED": "2"},
+                                 {"ACEDAG_K2": "tmem3"}, {"ACEDAG_K2": "tmem4"}, {"ACEDAG_TAIL_PARTS": "1"}])
 def test_kernel_variants_in_subprocess(cuda, env):
     """The alternative K2 geometries (32-site tiles, 16 warps, dynamic chunk
-    schedule, scalar multi-output) are selected once per process by
-    environment variables; each is checked against the oracle."""
+    schedule, scalar multi-output, four sites per lane with and without the
+    tile-major seed copy, last-round split off) are selected once per process
+    by environment variables; each is checked against the oracle."""
     import os
     import subprocess
     import sys

@@ -354,40 +354,30 @@ def run_ours(a):
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = P.launch_count()
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(a.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+    # our kernels launched inside the timed region (the library's own count)
+    gpu_launches = P.launch_count() - n_launch0
     barrier()
     torch.cuda.synchronize()
     ms_step = max_over_ranks(e0.elapsed_time(e1)) / a.steps
     value = global_sites / (ms_step * 1e-3)
 
-    # our kernels launched per step (pool chunks + K2 passes + reduce)
-    if pos:
-        chunks = (S + (1 << 17) - 1) >> 17
-        passes = 1 if n_out == 1 else (n_out + 31) // 32
-        per_step = chunks * (1 + passes) + 1
-    else:
-        per_step = 1
-    gpu_launches = per_step * a.steps
-
-    # kernel-only time of K2 (the dominant kernel) for the roofline
-    k2_ms = ms_step
-    if pos:
-        A_ws = P.pool_positions(cfg["D"], X[: min(S, 1 << 17)])
-        sub = A_ws.shape[0]
-        plan.evaluate(A_ws, result=torch.empty_like(out[:sub]))
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(3):
-            plan.evaluate(A_ws, result=torch.empty_like(out[:sub]) if n_out == 1 else out[:sub])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        k2_ms = e0.elapsed_time(e1) / 3 * S / sub
-        del A_ws
+    # per-phase device time of the K2 evaluations (CUDA events the library
+    # records on the launching stream around the seed copy and the K2 kernel)
+    nt = max(3, min(a.steps, 10))
+    plan.timing(True)
+    for _ in range(nt):
+        step()
+    ph = plan.read_timing()
+    plan.timing(False)
+    k2_ms = max_over_ranks(ph["main"] / nt)
+    phases = {"prep_ms": ph["prep"] / nt, "k2_ms": ph["main"] / nt, "post_ms": ph["post"] / nt}
 
     naive = None
     if not pos and not a.no_naive and a.prec == "f64":
@@ -454,11 +444,15 @@ def run_ours(a):
                 "flop_model": "F_site = 6 P_int + 3 L_f + 2 T n_out" + (" + 4 J U_used" if pos else "") + " (SURVEY.md 8d)"}
     roof["kernel"] = plan.kernel_name(prec=a.prec, sites=S)
     roof["kernel_ms"] = k2_ms
+    roof["step_share"] = k2_ms / ms_step
+    roof["phases_ms"] = phases
     prof = os.path.join(ROOT, "profiles", "r01", "traffic.json")
     roof["traffic"] = None
     if os.path.exists(prof):
         try:
-            roof["traffic"] = json.load(open(prof)).get(a.config)
+            ent = json.load(open(prof)).get(a.config)
+            if ent and ent.get("kernel") == roof.get("kernel"):
+                roof["traffic"] = ent["bytes"]
         except Exception:
             pass
 

@@ -137,6 +137,18 @@ int acedag_plan_program(const acedag_graph* g, const int64_t* node_ids,
                         int64_t* n_slots, void* ops, int64_t* n_ops,
                         int32_t* chunk, int64_t* stats);
 
+/* Kernels launched by this library since load (all plans and devices). */
+int64_t acedag_launch_count(void);
+
+/* Per-phase device timing of the evaluations on this plan (CUDA events on
+ * the launching stream): enable (1) / disable (0); both clear the record.
+ * _read synchronizes on the recorded events and returns the summed
+ * milliseconds of {seed preparation (tile-major copy), main K2 kernel,
+ * remainder (split-tail reduction)} and the number of evaluations, then
+ * clears the record. */
+int acedag_plan_timing(acedag_plan* plan, int enable);
+int acedag_plan_timing_read(acedag_plan* plan, double* ms3, int64_t* calls);
+
 /* Name of the kernel acedag_eval would launch for these arguments and S
  * sites (static string; "" and EINVAL on bad arguments).  For reporting. */
 const char* acedag_eval_kernel_name(const acedag_plan* plan, int method, int prec,

@@ -13,7 +13,8 @@ from .graph import (EvalGraph, GraphFormatError, GraphNode, UnsupportedVersionEr
                     build_graph, deserialize_graph, graph_from_parents, read_graph, seed_graph,
                     serialize_graph, write_graph)
 from .evaluator import (InvarianceReport, SitePlan, evaluate_graph, evaluate_model, invariance_check,
-                        invert_particles, naive_eval, naive_products, one_particle, pool, pool_batched,
+                        invert_particles, launch_count, naive_eval, naive_products, one_particle, pool,
+                        pool_batched,
                         pool_positions, random_particles, read_coefficients, read_particles,
                         rotate_particles, write_coefficients, write_particles)
 

@@ -53,6 +53,9 @@ SIGNATURES = {
     "acedag_check_coords": (C.c_int, [C.c_int, _dp, C.c_int64]),
     "acedag_pool_positions": (C.c_int, [C.c_int, _vp, _vp, C.c_int64, C.c_int32, C.c_double, C.c_double,
                                         _vp, _vp]),
+    "acedag_launch_count": (C.c_int64, []),
+    "acedag_plan_timing": (C.c_int, [_vp, C.c_int]),
+    "acedag_plan_timing_read": (C.c_int, [_vp, _vp, _vp]),
     "acedag_eval_host": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, _vp, _vp]),
     "acedag_eval_from_positions": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_double, C.c_double,
                                              C.c_int, _vp, _vp]),

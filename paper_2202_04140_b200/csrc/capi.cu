@@ -23,6 +23,14 @@
 #include "plan.h"
 #include "pool.cuh"
 
+#include <array>
+#include <atomic>
+namespace {
+// kernels this library launched (bench.py's gpu_launches; acedag_launch_count)
+std::atomic<int64_t> g_launches{0};
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace
+
 using namespace acedag;
 
 namespace {
@@ -332,6 +340,19 @@ struct acedag_plan {
   };
   std::mutex host_mu;
   HostPipe pipe;
+  // acedag_plan_timing: CUDA events around each eval's phases
+  // {start, after seed prep, after the main K2 kernel, end}
+  struct Timing {
+    bool on = false;
+    std::mutex mu;
+    std::vector<std::array<cudaEvent_t, 4>> ev;
+    void clear() {
+      for (auto& a : ev)
+        for (cudaEvent_t e : a) cudaEventDestroy(e);
+      ev.clear();
+    }
+    ~Timing() { clear(); }
+  } timing;
   Workspace* ws(cudaStream_t s) {
     std::lock_guard<std::mutex> lk(ws_mu);
     auto& w = wss[(void*)s];
@@ -616,6 +637,18 @@ constexpr int kNC = 8;
 // SMs a concurrent kernel of the same call keeps (the host-path seed gather
 // runs next to the persistent K2 grid); per thread so calls stay independent
 thread_local int t_sm_reserve = 0;
+// phase events of the eval being launched on this thread (acedag_plan_timing)
+thread_local cudaEvent_t* t_tev = nullptr;
+thread_local bool t_main_marked = false;
+void mark_prep(cudaStream_t st) {
+  if (t_tev) cudaEventRecord(t_tev[1], st);
+}
+void mark_main(cudaStream_t st) {
+  if (t_tev) {
+    cudaEventRecord(t_tev[2], st);
+    t_main_marked = true;
+  }
+}
 // CTAs of the host-path seed gather (ACEDAG_GATHER_CTAS overrides)
 int gather_ctas() {
   static int v = [] {
@@ -692,7 +725,7 @@ cudaError_t launch_fast_w(acedag_plan* P, const void* A, int64_t S, int L, const
   k<<<lc.grid, lc.block, lc.smem, st>>>(
       reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
       P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(lc.ws->gcache.p), lc.ws->part.p,
-      k2_sched());
+      k2_sched()); note_launch();
   return cudaGetLastError();
 }
 
@@ -714,7 +747,7 @@ cudaError_t launch_fast2_w(acedag_plan* P, const void* A, int64_t S, int L, cons
   if (e != cudaSuccess) return e;
   k<<<lc.grid, lc.block, lc.smem, st>>>(
       reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
-      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(lc.ws->gcache.p), lc.ws->part.p);
+      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(lc.ws->gcache.p), lc.ws->part.p); note_launch();
   return cudaGetLastError();
 }
 
@@ -758,7 +791,7 @@ cudaError_t launch_tmem_w(acedag_plan* P, const double2* A, int64_t S, int L, co
   e = lc.ws->part.alloc((size_t)lc.grid * WARPS * 32);
   if (e != cudaSuccess) return e;
   k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p);
+                                        out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
   return cudaGetLastError();
 }
 
@@ -799,7 +832,7 @@ cudaError_t launch_tmem2_w(acedag_plan* P, const double2* A, int64_t S, int L, c
   e = lc.ws->part.alloc((size_t)lc.grid * WARPS * 64);
   if (e != cudaSuccess) return e;
   k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p);
+                                        out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
   return cudaGetLastError();
 }
 
@@ -852,7 +885,7 @@ bool tile_seeds(acedag_plan* P, const double2* A, int64_t S, int L, const uint16
     if (e != cudaSuccess) return true;
     attr = true;
   }
-  dev::k_tile_seeds<TS><<<(unsigned)ntiles, 512, tsm, st>>>(A, S, L, cols, slots, P->U, ws->tiles.p);
+  dev::k_tile_seeds<TS><<<(unsigned)ntiles, 512, tsm, st>>>(A, S, L, cols, slots, P->U, ws->tiles.p); note_launch();
   e = cudaGetLastError();
   return true;
 }
@@ -865,6 +898,7 @@ cudaError_t launch_tmem3_k(acedag_plan* P, const double2* A, int64_t S, int L, c
   const bool tiled = tiled_mode() >= 2 && tile_seeds<64>(P, A, S, L, slot_label, lc.ws, st, e);
   if (tiled && e != cudaSuccess) return e;
   if (tiled) A = lc.ws->tiles.p;
+  mark_prep(st);
   auto k = tiled ? dev::k2_tmem3<NU, W, HYB, true> : dev::k2_tmem3<NU, W, HYB, false>;
   e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
@@ -879,11 +913,12 @@ cudaError_t launch_tmem3_k(acedag_plan* P, const double2* A, int64_t S, int L, c
     if (e != cudaSuccess) return e;
   }
   k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p);
+                                        out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p); note_launch();
+  mark_main(st);
   e = cudaGetLastError();
   if (e != cudaSuccess || parts == 1) return e;
   const int64_t rem = S - full * 64;
-  dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 64, S, 64, nchunks(P), out);
+  dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 64, S, 64, nchunks(P), out); note_launch();
   return cudaGetLastError();
 }
 
@@ -916,7 +951,7 @@ cudaError_t launch_tmem4_k(acedag_plan* P, const double2* A, int64_t S, int L, c
   e = lc.ws->part.alloc((size_t)lc.grid * W * 64);
   if (e != cudaSuccess) return e;
   k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops4.p, P->chunk.p, P->croots.p,
-                                        nchunks(P), out, lc.ws->gcache.p, lc.ws->part.p);
+                                        nchunks(P), out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
   return cudaGetLastError();
 }
 
@@ -941,6 +976,7 @@ cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, co
   const bool tiled = use_tiled() && tile_seeds<128>(P, A, S, L, slot_label, lc.ws, st, e);
   if (tiled && e != cudaSuccess) return e;
   if (tiled) A = lc.ws->tiles.p;
+  mark_prep(st);
   auto k = tiled ? (two ? dev::k2_quad<NU, W, 2, HYB, true> : dev::k2_quad<NU, W, 1, HYB, true>)
                  : (two ? dev::k2_quad<NU, W, 2, HYB, false> : dev::k2_quad<NU, W, 1, HYB, false>);
   e = set_smem(k, lc.smem);
@@ -956,11 +992,12 @@ cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, co
     if (e != cudaSuccess) return e;
   }
   k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->opsQ.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p);
+                                        out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p); note_launch();
+  mark_main(st);
   e = cudaGetLastError();
   if (e != cudaSuccess || parts == 1) return e;
   const int64_t rem = S - full * 128;
-  dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 128, S, 128, nchunks(P), out);
+  dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 128, S, 128, nchunks(P), out); note_launch();
   return cudaGetLastError();
 }
 
@@ -1058,7 +1095,7 @@ cudaError_t launch_multi(acedag_plan* P, const double2* A, int64_t S, int L, con
   if (e != cudaSuccess) return e;
   for (int o0 = 0; o0 < P->host.n_out; o0 += kNOC) {
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                          P->cre.p, P->host.n_out, o0, out, lc.ws->gcache.p, lc.ws->part.p);
+                                          P->cre.p, P->host.n_out, o0, out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -1077,7 +1114,7 @@ cudaError_t launch_mma(acedag_plan* P, const double2* A, int64_t S, int L, const
   if (e != cudaSuccess) return e;
   for (int o0 = 0; o0 < P->host.n_out; o0 += 32) {
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                          P->cre.p, P->host.n_out, o0, out, lc.ws->gcache.p, lc.ws->part.p);
+                                          P->cre.p, P->host.n_out, o0, out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -1104,7 +1141,7 @@ cudaError_t launch_general(acedag_plan* P, const double2* A, int64_t S, int L,
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p,
                                           nchunks(P), P->cre.p,
                                           P->host.complex_coef ? P->cim.p : nullptr, P->host.n_out, o0,
-                                          complex_out, out, lc.ws->gcache.p);
+                                          complex_out, out, lc.ws->gcache.p); note_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -1121,7 +1158,7 @@ cudaError_t launch_naive(acedag_plan* P, const double2* A, int64_t S, int L,
   for (int o0 = 0; o0 < P->host.n_out; ++o0) {
     k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->nseg.p, P->nslots.p,
                                           P->ncre.p, P->host.complex_coef ? P->ncim.p : nullptr,
-                                          P->host.n_out, o0, complex_out, out, lc.ws->gcache.p);
+                                          P->host.n_out, o0, complex_out, out, lc.ws->gcache.p); note_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -1187,7 +1224,28 @@ template <int NU> struct NaiveGen {
   }
 };
 
+int eval_body(acedag_plan* P, int method, int prec, int out_kind, const void* A, int64_t S, int L,
+              const uint16_t* slot_label, void* out, cudaStream_t st);
+
 int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A, int64_t S, int L,
+              const uint16_t* slot_label, void* out, cudaStream_t st) {
+  if (!P->timing.on) return eval_body(P, method, prec, out_kind, A, S, L, slot_label, out, st);
+  std::array<cudaEvent_t, 4> ev;
+  for (auto& e : ev) cudaEventCreate(&e);
+  cudaEventRecord(ev[0], st);
+  cudaEventRecord(ev[1], st);  // no seed-prep phase unless the launcher marks one
+  t_tev = ev.data();
+  t_main_marked = false;
+  const int rc = eval_body(P, method, prec, out_kind, A, S, L, slot_label, out, st);
+  if (!t_main_marked) cudaEventRecord(ev[2], st);
+  cudaEventRecord(ev[3], st);
+  t_tev = nullptr;
+  std::lock_guard<std::mutex> lk(P->timing.mu);
+  P->timing.ev.push_back(ev);
+  return rc;
+}
+
+int eval_body(acedag_plan* P, int method, int prec, int out_kind, const void* A, int64_t S, int L,
               const uint16_t* slot_label, void* out, cudaStream_t st) {
   const PlanHost& H = P->host;
   const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
@@ -1350,6 +1408,7 @@ int acedag_eval_host(const acedag_plan* Pc, int method, int prec, int out_kind, 
         dev::k_gather_seeds<float2><<<gather_ctas(), 512, U * 4, H.sg>>>(
             reinterpret_cast<const float2*>(src) + s0 * L, n, L, P->sorted_labels.p, U,
             reinterpret_cast<float2*>(H.buf[b].p));
+      note_launch();
       e = cudaGetLastError();
     } else {
       e = cudaMemcpyAsync(H.buf[b].p, src + (size_t)s0 * L * esz, (size_t)n * L * esz, cudaMemcpyHostToDevice, H.sg);
@@ -1386,6 +1445,36 @@ int acedag_eval_host(const acedag_plan* Pc, int method, int prec, int out_kind, 
   return ACEDAG_OK;
 }
 
+int64_t acedag_launch_count(void) { return g_launches.load(); }
+
+int acedag_plan_timing(acedag_plan* P, int enable) {
+  if (!P) return fail(ACEDAG_EINVAL, "plan is NULL");
+  DevGuard dg(P->device);
+  std::lock_guard<std::mutex> lk(P->timing.mu);
+  P->timing.clear();
+  P->timing.on = enable != 0;
+  return ACEDAG_OK;
+}
+
+int acedag_plan_timing_read(acedag_plan* P, double* ms, int64_t* calls) {
+  if (!P || !ms) return fail(ACEDAG_EINVAL, "NULL argument");
+  DevGuard dg(P->device);
+  std::lock_guard<std::mutex> lk(P->timing.mu);
+  ms[0] = ms[1] = ms[2] = 0.0;
+  for (auto& a : P->timing.ev) {
+    cudaError_t e = cudaEventSynchronize(a[3]);
+    if (e != cudaSuccess) return cuda_fail(e, "timing events");
+    for (int k = 0; k < 3; ++k) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, a[k], a[k + 1]);
+      ms[k] += t;
+    }
+  }
+  if (calls) *calls = (int64_t)P->timing.ev.size();
+  P->timing.clear();
+  return ACEDAG_OK;
+}
+
 const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, int out_kind, int64_t S) {
   if (!P || !P->has_coef) {
     fail(ACEDAG_EINVAL, "plan has no coefficients");
@@ -1417,7 +1506,7 @@ int acedag_reduce_sites(const acedag_plan* P, const double* phi, int64_t S, doub
   if (!P || !out_total || (S > 0 && !phi)) return fail(ACEDAG_EINVAL, "NULL argument");
   if (!P->has_coef) return fail(ACEDAG_EINVAL, "plan has no coefficients");
   DevGuard dg(P->device);
-  dev::k_reduce_sites<<<P->host.n_out, 1024, 0, (cudaStream_t)stream>>>(phi, S, P->host.n_out, out_total);
+  dev::k_reduce_sites<<<P->host.n_out, 1024, 0, (cudaStream_t)stream>>>(phi, S, P->host.n_out, out_total); note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "k_reduce_sites");
   return ACEDAG_OK;
@@ -1429,7 +1518,7 @@ int acedag_naive_products(const double* vals, const int32_t* lens, int64_t n, in
   if (n == 0) return ACEDAG_OK;
   int grid = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
   dev::k_naive_products<<<grid, 128, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const double2*>(vals), lens, n, width, reinterpret_cast<double2*>(out));
+      reinterpret_cast<const double2*>(vals), lens, n, width, reinterpret_cast<double2*>(out)); note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "k_naive_products");
   return ACEDAG_OK;
@@ -1443,7 +1532,7 @@ int acedag_eval_nodes(const acedag_plan* P, const double* A, int64_t S, double* 
   const int L = (int)P->g->n_seeds();
   int grid = (int)std::min<int64_t>((S + 127) / 128, (int64_t)P->sms * 16);
   dev::k_eval_nodes<<<grid, 128, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const double2*>(A), S, L, N, P->pa.p, P->pb.p, reinterpret_cast<double2*>(node_vals));
+      reinterpret_cast<const double2*>(A), S, L, N, P->pa.p, P->pb.p, reinterpret_cast<double2*>(node_vals)); note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "k_eval_nodes");
   return ACEDAG_OK;
@@ -1488,10 +1577,10 @@ int acedag_pool(int group, int cap, const double* coords, const int32_t* counts,
   cudaStream_t st = (cudaStream_t)stream;
   double2* out = reinterpret_cast<double2*>(A_out);
   switch (group) {
-    case 0: dev::pool_ref<0><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); break;
-    case 1: dev::pool_ref<1><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); break;
-    case 2: dev::pool_ref<2><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); break;
-    default: dev::pool_ref<3><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); break;
+    case 0: dev::pool_ref<0><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); note_launch(); break;
+    case 1: dev::pool_ref<1><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); note_launch(); break;
+    case 2: dev::pool_ref<2><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); note_launch(); break;
+    default: dev::pool_ref<3><<<grid, 256, 0, st>>>(coords, counts, S, J, labels, L, out); note_launch(); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pool_ref");
@@ -1528,7 +1617,7 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
   }
   CK(cudaFuncSetAttribute(dev::pool_positions2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dev::pool_positions2<<<grid, 256, smem, st>>>(xyz, counts, S, J, cap, r_in, r_cut, tri, ntri, col_of,
-                                                stride, out);
+                                                stride, out); note_launch();
   (void)labels;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pool_positions");

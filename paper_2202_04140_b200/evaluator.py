@@ -162,6 +162,19 @@ class SitePlan:
         self.complex_coef = cplx
         return self
 
+    def timing(self, enable: bool = True) -> None:
+        """Record per-phase CUDA-event timings of subsequent evaluations."""
+        N.check(N.lib().acedag_plan_timing(self._h, 1 if enable else 0))
+
+    def read_timing(self) -> dict:
+        """Summed device milliseconds per phase since timing() / the last
+        read: ``prep`` (tile-major seed copy), ``main`` (the K2 kernel),
+        ``post`` (split-tail reduction); ``calls`` evaluations."""
+        ms = (C.c_double * 3)()
+        calls = C.c_int64()
+        N.check(N.lib().acedag_plan_timing_read(self._h, ms, C.byref(calls)))
+        return {"prep": ms[0], "main": ms[1], "post": ms[2], "calls": calls.value}
+
     def kernel_name(self, method: str = "recursive", prec: str = "f64", out: str = "real",
                     sites: int = 1 << 20) -> str:
         """The kernel evaluate() launches for these arguments on ``sites``
@@ -315,6 +328,11 @@ class SitePlan:
             total = torch.zeros(self.n_out, dtype=torch.float64, device=phi.device)
         N.check(N.lib().acedag_reduce_sites(self._h, _vp(phi), phi.shape[0], _vp(total), _stream(phi.device)))
         return total
+
+
+def launch_count() -> int:
+    """Kernels the native library has launched since it was loaded."""
+    return int(N.lib().acedag_launch_count())
 
 
 def naive_products(vals: torch.Tensor, lens: torch.Tensor | None = None) -> torch.Tensor:

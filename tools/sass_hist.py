@@ -9,6 +9,8 @@ from collections import Counter
 
 def main(path, top=40):
     rows = list(csv.reader(open(path)))
+    cut = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+    rows = rows[: cut[1]] if len(cut) > 1 else rows  # first kernel only
     hdr = rows[1]
     ia, ie, ist = hdr.index("Source"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
     ops, stalls, total, seq = Counter(), Counter(), 0, []
@@ -18,6 +20,8 @@ def main(path, top=40):
         src = r[ia].strip()
         m = re.match(r"(@!?U?P\w+\s+)?([A-Z0-9_]+)", src)
         if not m:
+            continue
+        if not (r[ie] or "0").isdigit():
             continue
         n = int(r[ie] or 0)
         op = m.group(2)

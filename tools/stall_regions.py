@@ -6,6 +6,8 @@ import sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
+cut = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+rows = rows[: cut[1]] if len(cut) > 1 else rows  # first kernel only
 hdr = rows[1]
 ie = hdr.index("Instructions Executed")
 reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
@@ -14,6 +16,8 @@ agg = defaultdict(lambda: defaultdict(int))
 tot = defaultdict(int)
 for r in rows[2:]:
     if len(r) <= max(idx):
+        continue
+    if not (r[ie] or "0").isdigit():
         continue
     ex = int(r[ie] or 0)
     for name, i in zip(reasons, idx):

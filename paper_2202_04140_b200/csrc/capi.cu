@@ -20,6 +20,7 @@
 #include "../../include/acedag_b200.h"
 #include "graph.h"
 #include "kernels.cuh"
+#include "horner.h"
 #include "plan.h"
 #include "pool.cuh"
 
@@ -298,6 +299,10 @@ struct acedag_plan {
   DevBuf<int4> tri;        // (n, l, m >= 0) triples the used labels need
   DevBuf<Op> ops;
   DevBuf<Op> opsQ;         // k2_quad: hot counts for its 32 TMEM slots
+  DevBuf<OpH> opsH;        // k2_horner encoding (encode_horner), if it fits
+  DevBuf<int32_t> crootsH, chunkH;
+  bool opsH_ok = false;
+  int usH = 0;             // k2_horner shared-memory rows
   DevBuf<Op> ops4;         // k2_tmem4 encoding (encode_ops4), if it fits
   DevBuf<int32_t> croots;  // roots per chunk
   bool ops4_ok = false;
@@ -559,7 +564,20 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   }
   CK(P->ops.upload(H.ops));
   CK(P->chunk.upload(H.chunk));
-  if (k2_mode() == 5 || k2_mode() == 7) CK(P->opsQ.upload(reencode_hot(H, dev::kTmemRowsQ)));
+  if (k2_mode() == 5 || k2_mode() == 7 || k2_mode() == 9) CK(P->opsQ.upload(reencode_hot(H, dev::kTmemRowsQ)));
+  P->opsH_ok = false;
+  if ((k2_mode() == 5 || k2_mode() == 9) && H.max_order <= 4) {
+    const int hot = std::min(P->U, (int)kHornerHot);
+    P->usH = std::min(P->U - hot, horner_us_max(P->smem_optin));
+    std::vector<OpH> oh;
+    std::vector<int32_t> ch, cr;
+    P->opsH_ok = encode_horner(H, (uint32_t)hot, (uint32_t)P->usH, oh, ch, cr);
+    if (P->opsH_ok) {
+      CK(P->opsH.upload(oh));
+      CK(P->chunkH.upload(ch));
+      CK(P->crootsH.upload(cr));
+    }
+  }
   if (k2_mode() == 6) {
     const int rows = P->U + 1, cold = std::max(0, rows - (int)dev::kTmemRows2);
     std::vector<Op> o4;
@@ -776,6 +794,7 @@ int k2_mode() {
     if (e && std::string(e) == "tmem4") return 6;
     if (e && std::string(e) == "quad") return 7;
     if (e && std::string(e) == "tmem3") return 8;
+    if (e && std::string(e) == "horner") return 9;
     if (k2_spl_env() == 1) return 1;
     return 5;
   }();
@@ -999,6 +1018,44 @@ cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, co
   const int64_t rem = S - full * 128;
   dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 128, S, 128, nchunks(P), out); note_launch();
   return cudaGetLastError();
+}
+
+// k2_horner on the tile-major seed table; false (nothing launched) when the
+// input layout is not one tile_seeds knows
+bool run_horner(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label, double* out,
+                Launch& lc, cudaStream_t st, cudaError_t& e) {
+  if (!tile_seeds<128>(P, A, S, L, slot_label, lc.ws, st, e)) return false;
+  if (e != cudaSuccess) return true;
+  mark_prep(st);
+  const int64_t ntiles = (S + 127) / 128;
+  // fewer tiles than SMs: the grid covers program slices of them too
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles * 8, P->sms - t_sm_reserve));
+  const int nch = nchunks(P);
+  e = lc.ws->part.alloc((size_t)grid * nch * 128);
+  if (e != cudaSuccess) return true;
+  int64_t full = ntiles;
+  int parts = 1;
+  tail_split(ntiles, grid, nch, full, parts);
+  if (parts > 1) {
+    e = lc.ws->tail.alloc((size_t)(ntiles - full) * nch * 128);
+    if (e != cudaSuccess) return true;
+  }
+  e = launch_horner(P->host.max_order, lc.ws->tiles.p, S, P->U, P->usH, P->opsH.p, P->chunkH.p, P->crootsH.p, nch,
+                    out, lc.ws->part.p, full, parts, lc.ws->tail.p, grid, st);
+  note_launch();
+  mark_main(st);
+  if (e != cudaSuccess || parts == 1) return true;
+  const int64_t rem = S - full * 128;
+  dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 128, S, 128, nch, out);
+  note_launch();
+  e = cudaGetLastError();
+  return true;
+}
+
+// auto selection (k2_mode 5) prefers k2_horner where k2_quad would run
+bool use_horner(const acedag_plan* P, int64_t S) {
+  (void)S;  // every batch size, so a site's value never depends on its batch
+  return P->opsH_ok && P->host.max_order <= 4 && (k2_mode() == 9 || k2_mode() == 5);
 }
 
 template <int NU> struct QuadF64 {
@@ -1264,7 +1321,10 @@ int eval_body(acedag_plan* P, int method, int prec, int out_kind, const void* A,
         if (rc) return rc;
         e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
       }
-    } else if (fast && (k2_mode() == 7 || (k2_mode() == 5 && use_quad(P, S)))) {
+    } else if (fast && use_horner(P, S) &&
+               run_horner(P, (const double2*)A, S, L, slot_label, (double*)out, lc, st, e)) {
+      if (e != cudaSuccess) return cuda_fail(e, "k2_horner");
+    } else if (fast && (k2_mode() == 7 || k2_mode() == 9 || (k2_mode() == 5 && use_quad(P, S)))) {
       int rc = quad_launch(P, S, lc);
       if (rc) return rc;
       e = by_order<QuadF64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
@@ -1489,7 +1549,8 @@ const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, 
       case 8: return "k2_tmem3";
       case 7: return "k2_quad";
       case 6: return P->ops4_ok ? "k2_tmem4" : "k2_tmem3";
-      case 5: return use_quad(P, S) ? "k2_quad" : "k2_tmem3";
+      case 5: return use_horner(P, S) ? "k2_horner" : (use_quad(P, S) ? "k2_quad" : "k2_tmem3");
+      case 9: return use_horner(P, S) ? "k2_horner" : "k2_quad";
       case 4: return "k2_tmem2";
       case 3: return "k2_tmem";
       case 2: return "k2_fast2";

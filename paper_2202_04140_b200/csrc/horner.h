@@ -1,0 +1,59 @@
+// K2 Horner kernel (k2_horner): host-side encoding and launcher.
+//
+// The recursive program of plan.h evaluated bottom-up.  For a plan node u
+// with value V_u (product of the seeds on its path) define
+//     H_u = c_u + sum_{children q} s_q * H_q        (s_q: the child's seed)
+// so that sum_{w in subtree(u)} c_w V_w = V_u * H_u and
+//     phi = sum_roots Re(s_a * s_b * H_root).
+// A leaf costs one complex FMA of a real coefficient (2 DFMA per site)
+// instead of a product and a dot (3 DP instructions); an inner node one
+// complex multiply-add (4 DFMA) instead of 5.  Node values are never formed;
+// the node set and coefficients are exactly those of the plan, so the result
+// equals evaluate_model's to rounding (evaluator.py:124-142).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "plan.h"
+
+namespace acedag {
+
+// 16-byte record, read warp-uniformly.  z: the seed's class-scaled offset
+// (TMEM row -> column row*16; shared row -> byte row*2048; global row -> byte
+// row*2048).  w: nch | nhot << 16 | nsm << 22 (children by class, in that
+// order).  A root is two records; the second carries w = cls_a | cls_b << 2 |
+// single << 4 (single: an order-1 coefficient, phi += c Re(s_a)).
+struct alignas(16) OpH {
+  double c;
+  uint32_t z;
+  uint32_t w;
+};
+
+constexpr uint32_t kHornerHot = 32;      // TMEM rows (4 sites x c128 = 16 columns each)
+constexpr int kHornerWarps = 16;
+constexpr uint32_t kHornerRing = 2048;   // per-warp program ring: 3 blocks + mirror
+// leaves per record group: a node of the last inner order with more is split
+// into copies of the same seed (the first carrying its coefficient), so a
+// node and its leaves always fit the 32-record ring window
+constexpr uint32_t kMaxLeaves = 30;
+
+// Re-encodes the plan's DFS program for k2_horner with `hot` TMEM rows and
+// `us` shared-memory rows (slot order: hot, shared, global), chunked like the
+// plan: chunk gets each chunk's first record, croots its number of roots.
+// Returns false when a count does not fit its field (another kernel is used).
+bool encode_horner(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<OpH>& out,
+                   std::vector<int32_t>& chunk, std::vector<int32_t>& croots);
+
+// shared-memory rows k2_horner can hold besides its rings
+int horner_us_max(size_t smem_optin);
+size_t horner_smem(int us);
+
+// tiles: tile-major seed table [ntiles][U+1][128] c128 (k_tile_seeds<128>).
+// part: [grid][nchunk][128]; tail: [(ntiles - full)][nchunk][128].
+cudaError_t launch_horner(int nu, const double2* tiles, int64_t S, int U, int us, const OpH* ops,
+                          const int32_t* chunk, const int32_t* croots, int nchunk, double* out, double* part,
+                          int64_t full, int parts, double* tail, int grid, cudaStream_t st);
+
+}  // namespace acedag

@@ -261,8 +261,8 @@ def test_host_pipelines_match_device(cuda, cfg2, golden):
 
 def test_batch_independent_results(cuda, cfg2):
     """A site's phi does not depend on the batch it is evaluated in: the
-    default kernels sum one partial per program chunk in chunk order, so the
-    tile geometry (k2_quad / k2_tmem3), the last-round split and the site
+    default kernel (k2_horner for order <= 4) sums one partial per program
+    chunk in chunk order, so the grid, the last-round split and the site
     count leave every value bit-identical."""
     c = np.random.default_rng(34).normal(size=len(cfg2.target_ids))
     plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
@@ -297,7 +297,8 @@ def test_eval_host_variants(cuda, cfg2):
 @pytest.mark.parametrize("env", [{"ACEDAG_K2_SPL": "1"}, {"ACEDAG_K2": "tmem2"}, {"ACEDAG_K2_SPL": "1", "ACEDAG_K2_WARPS": "16"},
                                  {"ACEDAG_SCHED": "1"}, {"ACEDAG_MULTI": "scalar"}, {"ACEDAG_K2": "quad"},
                                  {"ACEDAG_K2": "quad", "ACEDAG_TILED": "0"}, {"ACEDAG_TILED": "2"},
-                                 {"ACEDAG_K2": "tmem3"}, {"ACEDAG_K2": "tmem4"}, {"ACEDAG_TAIL_PARTS": "1"}])
+                                 {"ACEDAG_K2": "tmem3"}, {"ACEDAG_K2": "tmem4"}, {"ACEDAG_TAIL_PARTS": "1"},
+                                 {"ACEDAG_K2": "horner"}, {"ACEDAG_K2": "horner", "ACEDAG_TILED": "0"}])
 def test_kernel_variants_in_subprocess(cuda, env):
     """The alternative K2 geometries (32-site tiles, 16 warps, dynamic chunk
     schedule, scalar multi-output, four sites per lane with and without the

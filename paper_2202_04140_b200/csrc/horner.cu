@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <vector>
 
@@ -201,16 +202,38 @@ __device__ __forceinline__ C4 seed_of(const SeedsH<HYB>& sd, uint32_t z) {
 }
 
 // the leaves (maximum order) of one node, records from q: hot, shared,
-// global (at most kMaxLeaves, so they lie in the checked ring window)
+// global (at most kMaxLeaves, so they lie in the checked ring window).  Hot
+// leaves go two per TMEM round trip; a node whose leaves are all hot (the
+// usual case) skips the other loops.
 template <bool HYB>
-__device__ __forceinline__ void leaves(uint32_t q, uint32_t w, C4& H, const SeedsH<HYB>& sd) {
-  const uint32_t nh = w_nhot(w), ns = w_nsm(w);
-  const uint32_t qh = q + nh * 16, qs = qh + ns * 16, qe = q + w_nch(w) * 16;
+__device__ __forceinline__ void hot_leaves(uint32_t q, uint32_t qh, C4& H, const SeedsH<HYB>& sd) {
 #pragma unroll 1
-  for (; q < qh; q += 16) {
+  for (; q + 16 < qh; q += 32) {
+    const int4 r0 = lds128(q), r1 = lds128(q + 16);
+    uint32_t t0[16], t1[16];
+    sd.hot((uint32_t)r0.z, t0);
+    sd.hot((uint32_t)r1.z, t1);
+    tmem_wait_ld();
+    axpy(H, rec_c(r0), SeedsH<HYB>::unpack(t0));
+    axpy(H, rec_c(r1), SeedsH<HYB>::unpack(t1));
+  }
+  if (q < qh) {
     const int4 r = lds128(q);
     axpy(H, rec_c(r), seed_of<0, HYB>(sd, (uint32_t)r.z));
   }
+}
+
+template <bool HYB>
+__device__ __forceinline__ void leaves(uint32_t q, uint32_t w, C4& H, const SeedsH<HYB>& sd) {
+  const uint32_t nh = w_nhot(w), ns = w_nsm(w), n = w_nch(w);
+  const uint32_t qh = q + nh * 16;
+  if (nh == n) {
+    hot_leaves<HYB>(q, qh, H, sd);
+    return;
+  }
+  const uint32_t qs = qh + ns * 16, qe = q + n * 16;
+  hot_leaves<HYB>(q, qh, H, sd);
+  q = qh;
 #pragma unroll 1
   for (; q < qs; q += 16) {
     const int4 r = lds128(q);
@@ -327,13 +350,12 @@ __device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<H
 }
 
 // T: tile-major seed table [ntiles][U + 1][128] c128
-template <int NU, bool HYB>
-__global__ void __launch_bounds__(kHornerWarps * 32, 1)
+template <int NU, bool HYB, int W>
+__global__ void __launch_bounds__(W * 32, 1)
 k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __restrict__ ops,
           const int32_t* __restrict__ chunk, const int32_t* __restrict__ croots, int nchunk,
           double* __restrict__ out, double* __restrict__ part, int64_t full_tiles, int tail_parts,
           double* __restrict__ tailbuf) {
-  constexpr int W = kHornerWarps;
   unsigned char* smem = h_smem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rows = U + 1;  // table rows (row U: the constant ONE, unused here)
@@ -367,6 +389,19 @@ k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __
     const int nsl = whole ? 1 : tail_parts;
     const int cb = (int)((int64_t)slice * nchunk / nsl), ce = (int)((int64_t)(slice + 1) * nchunk / nsl);
     const double2* Tt = T + tile * (int64_t)rows * 128;
+    // the next item's on-chip rows into L2 while this tile computes
+    if (threadIdx.x == 0 && it + gridDim.x < nitems) {
+      const int64_t nit = it + gridDim.x;
+      const int64_t nt = nit < full_tiles ? nit : full_tiles + (nit - full_tiles) / tail_parts;
+      if (nt != tile) {
+        const char* src = reinterpret_cast<const char*>(T + nt * (int64_t)rows * 128);
+        const uint32_t bytes = (uint32_t)(hot + us) * 2048u;
+        for (uint32_t o = 0; o < bytes; o += 32768u) {
+          const uint32_t n = bytes - o < 32768u ? bytes - o : 32768u;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src + o), "r"(n) : "memory");
+        }
+      }
+    }
     if (HYB) sd.gb = reinterpret_cast<const char*>(Tt + (size_t)(hot + us) * 128) + lane * 16;
     // TMEM rows: each lane quadrant's four warps write all hot rows
     for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (W / 4)) {
@@ -432,13 +467,33 @@ k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __
 }  // namespace hdev
 
 // ------------------------------------------------------------------- host
+// warps per CTA (ACEDAG_HWARPS = 16 | 20 | 24)
+int horner_warps() {
+  static int w = [] {
+    const char* e = getenv("ACEDAG_HWARPS");
+    const int v = e ? atoi(e) : kHornerWarps;
+    return v == 20 || v == 24 ? v : 16;
+  }();
+  return w;
+}
+
 int horner_us_max(size_t smem_optin) {
-  const size_t fixed = (size_t)kHornerWarps * kHornerRing + 16;
+  const size_t fixed = (size_t)horner_warps() * kHornerRing + 16;
   return smem_optin > fixed ? (int)((smem_optin - fixed) / 2048) : 0;
 }
-size_t horner_smem(int us) { return (size_t)us * 2048 + (size_t)kHornerWarps * kHornerRing + 16; }
+size_t horner_smem(int us) { return (size_t)us * 2048 + (size_t)horner_warps() * kHornerRing + 16; }
 
 namespace {
+uint32_t w_count(uint32_t w) { return w & 0xFFFFu; }
+// relative size of the second half of the chunks (ACEDAG_HGUIDE; 1 = equal)
+double guided_tail() {
+  static double v = [] {
+    const char* e = getenv("ACEDAG_HGUIDE");
+    const double x = e ? atof(e) : 1.0;
+    return x > 0 ? x : 1.0;
+  }();
+  return v;
+}
 struct HornerEnc {
   const PlanHost& H;
   uint32_t hot, us, U;
@@ -558,15 +613,51 @@ bool encode_horner(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<OpH
                    std::vector<int32_t>& chunk, std::vector<int32_t>& croots) {
   out.clear();
   const size_t nchunk = H.chunk.size() > 0 ? H.chunk.size() - 1 : 0;
-  chunk.assign(nchunk + 1, 0);
-  croots.assign(nchunk, 0);
   HornerEnc E{H, hot, us, (uint32_t)H.slot_label.size(), H.max_order, out};
+  // every root unit (a split root is several), with its record offset and cost
+  std::vector<size_t> start;
+  std::vector<double> cost;
+  {
+    size_t i = 0;
+    while (i < H.ops.size()) {
+      const size_t b0 = out.size();
+      const int32_t r0 = E.nroots;
+      i = E.root(i);
+      // the units the root became (a split NU=3 root: consecutive pair + leaves)
+      size_t q = b0;
+      for (int32_t k = r0; k < E.nroots; ++k) {
+        const size_t e = E.nroots - r0 == 1 ? out.size() : q + 2 + w_count(out[q].w);
+        start.push_back(q);
+        double c = 2.0;
+        for (size_t t = q; t < e; ++t) c += (t != q + 1 && out[t].w) ? 3.0 : 1.0;
+        cost.push_back(c);
+        q = e;
+      }
+    }
+  }
+  // guided chunking: the first half of the chunks take a share `big` of the
+  // work each, the second half a quarter of that, so the last chunks a warp
+  // grabs in a tile are short and the tile-end barrier waits less
+  const size_t nu = start.size();
+  double total = 0;
+  for (double c : cost) total += c;
+  std::vector<double> wt(nchunk);
+  double wsum = 0;
+  for (size_t i = 0; i < nchunk; ++i) wsum += (wt[i] = i < nchunk / 2 ? 1.0 : guided_tail());
+  chunk.assign(nchunk + 1, (int32_t)out.size());
+  croots.assign(nchunk, 0);
+  chunk[0] = 0;
+  size_t u = 0;
+  double acc = 0, target = 0;
   for (size_t ci = 0; ci < nchunk; ++ci) {
-    chunk[ci] = (int32_t)out.size();
-    E.nroots = 0;
-    size_t i = (size_t)H.chunk[ci];
-    while (i < (size_t)H.chunk[ci + 1]) i = E.root(i);
-    croots[ci] = E.nroots;
+    chunk[ci] = (int32_t)(u < nu ? start[u] : out.size());
+    target += wt[ci] / wsum * total;
+    int32_t nr = 0;
+    while (u < nu && (acc + 0.5 * cost[u] <= target || ci + 1 == nchunk)) {
+      acc += cost[u++];
+      nr++;
+    }
+    croots[ci] = nr;
   }
   chunk[nchunk] = (int32_t)out.size();
   return E.ok && out.size() < (size_t)INT32_MAX;
@@ -576,11 +667,12 @@ template <int NU, bool HYB>
 static cudaError_t launch_nu(const double2* T, int64_t S, int U, int us, const OpH* ops, const int32_t* chunk,
                              const int32_t* croots, int nchunk, double* out, double* part, int64_t full, int parts,
                              double* tail, int grid, cudaStream_t st) {
-  auto k = hdev::k2_horner<NU, HYB>;
+  const int W = horner_warps();
+  auto k = W == 24 ? hdev::k2_horner<NU, HYB, 24> : (W == 20 ? hdev::k2_horner<NU, HYB, 20> : hdev::k2_horner<NU, HYB, 16>);
   const size_t smem = horner_smem(us);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, kHornerWarps * 32, smem, st>>>(T, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail);
+  k<<<grid, W * 32, smem, st>>>(T, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail);
   return cudaGetLastError();
 }
 

@@ -201,10 +201,16 @@ __device__ __forceinline__ C4 seed_of(const SeedsH<HYB>& sd, uint32_t z) {
   }
 }
 
-// the leaves (maximum order) of one node, records from q: hot, shared,
-// global (at most kMaxLeaves, so they lie in the checked ring window).  Hot
-// leaves go two per TMEM round trip; a node whose leaves are all hot (the
-// usual case) skips the other loops.
+// H = c + c_l s (the accumulator's first term folded into its FMAs)
+__device__ __forceinline__ void axpy_init(C4& H, double c, double cl, const C4& s) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    H.v[k].x = __fma_rn(cl, s.v[k].x, c);
+    H.v[k].y = __dmul_rn(cl, s.v[k].y);
+  }
+}
+
+// hot leaves [q, qh) two per TMEM round trip
 template <bool HYB>
 __device__ __forceinline__ void hot_leaves(uint32_t q, uint32_t qh, C4& H, const SeedsH<HYB>& sd) {
 #pragma unroll 1
@@ -223,17 +229,27 @@ __device__ __forceinline__ void hot_leaves(uint32_t q, uint32_t qh, C4& H, const
   }
 }
 
+// H = c + sum over the leaves (maximum order) of one node, whose records
+// start at q (first: l, already read): hot, shared, global -- at most
+// kMaxLeaves, so they lie in the checked ring window.  The first leaf's FMA
+// carries c; a node whose leaves are all hot (the usual case) skips the
+// other loops.
 template <bool HYB>
-__device__ __forceinline__ void leaves(uint32_t q, uint32_t w, C4& H, const SeedsH<HYB>& sd) {
+__device__ __forceinline__ void leaves(uint32_t q, uint32_t w, double c, int4 l, C4& H, const SeedsH<HYB>& sd) {
   const uint32_t nh = w_nhot(w), ns = w_nsm(w), n = w_nch(w);
-  const uint32_t qh = q + nh * 16;
-  if (nh == n) {
-    hot_leaves<HYB>(q, qh, H, sd);
+  const uint32_t qh = q + nh * 16, qs = qh + ns * 16, qe = q + n * 16;
+  if (nh) {
+    axpy_init(H, c, rec_c(l), seed_of<0, HYB>(sd, (uint32_t)l.z));
+    hot_leaves<HYB>(q + 16, qh, H, sd);
+    if (nh == n) return;
+    q = qh;
+  } else if (n) {
+    axpy_init(H, c, rec_c(l), ns ? sd.sm((uint32_t)l.z) : sd.gl((uint32_t)l.z));
+    q += 16;
+  } else {
+    init_h(H, c);
     return;
   }
-  const uint32_t qs = qh + ns * 16, qe = q + n * 16;
-  hot_leaves<HYB>(q, qh, H, sd);
-  q = qh;
 #pragma unroll 1
   for (; q < qs; q += 16) {
     const int4 r = lds128(q);
@@ -259,7 +275,6 @@ __device__ __forceinline__ void parents(RingH& st, uint32_t n, C4& Hp, const See
     const int4 r = st.at(0), l = st.at(1);
     const uint32_t w = (uint32_t)r.w;
     C4 H, sp;
-    init_h(H, rec_c(r));
     if (w == (1u | 1u << 16)) {  // one hot leaf (the commonest shape)
       uint32_t tl[16];
       sd.hot((uint32_t)l.z, tl);
@@ -271,9 +286,9 @@ __device__ __forceinline__ void parents(RingH& st, uint32_t n, C4& Hp, const See
       } else {
         tmem_wait_ld();
       }
-      axpy(H, rec_c(l), SeedsH<HYB>::unpack(tl));
+      axpy_init(H, rec_c(r), rec_c(l), SeedsH<HYB>::unpack(tl));
     } else {
-      leaves<HYB>(st.p + 16, w, H, sd);
+      leaves<HYB>(st.p + 16, w, rec_c(r), l, H, sd);
       if constexpr (PC == 0) sp = seed_of<0, HYB>(sd, (uint32_t)r.z);
     }
     if constexpr (PC != 0) sp = seed_of<PC, HYB>(sd, (uint32_t)r.z);
@@ -323,12 +338,12 @@ __device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<H
   const double c = rec_c(r0);
   const uint32_t fl = (uint32_t)r1.w;
   C4 H;
-  init_h(H, c);
   if constexpr (NU == 3) {
-    leaves<HYB>(st.p + 32, (uint32_t)r0.w, H, sd);
+    leaves<HYB>(st.p + 32, (uint32_t)r0.w, c, st.at(2), H, sd);
     st.p += 16 * (2 + w_nch((uint32_t)r0.w));
     st.check(lane);
   } else {
+    init_h(H, c);
     st.p += 32;
     st.check(lane);
     if constexpr (NU >= 4) children<3, NU, HYB>(st, (uint32_t)r0.w, H, sd, lane);

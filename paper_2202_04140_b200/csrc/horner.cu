@@ -126,7 +126,9 @@ struct SeedsH {
   uint32_t tq;     // TMEM address of this warp's lane quadrant, column 0
   uint32_t sb;     // shared address of cold row 0 + lane * 16
   const char* gb;  // global tail row 0 of this tile + lane * 16
-  __device__ __forceinline__ void hot(uint32_t z, uint32_t (&t)[16]) const { tmem_ld16(tq + z, t); }
+  // z: TMEM address of the row in this warp's lane quadrant (the program
+  // copy of the quadrant carries the lane bits; the allocation base is 0)
+  __device__ __forceinline__ void hot(uint32_t z, uint32_t (&t)[16]) const { tmem_ld16(z, t); }
   __device__ __forceinline__ static C4 unpack(const uint32_t (&t)[16]) {
     C4 s;
 #pragma unroll
@@ -287,6 +289,21 @@ __device__ __forceinline__ void parents(RingH& st, uint32_t n, C4& Hp, const See
         tmem_wait_ld();
       }
       axpy_init(H, rec_c(r), rec_c(l), SeedsH<HYB>::unpack(tl));
+    } else if (w == (2u | 2u << 16)) {  // two hot leaves (the next commonest)
+      const int4 l2 = st.at(2);
+      uint32_t tl[16], tl2[16];
+      sd.hot((uint32_t)l.z, tl);
+      sd.hot((uint32_t)l2.z, tl2);
+      if constexpr (PC == 0) {
+        uint32_t tp[16];
+        sd.hot((uint32_t)r.z, tp);
+        tmem_wait_ld();
+        sp = SeedsH<HYB>::unpack(tp);
+      } else {
+        tmem_wait_ld();
+      }
+      axpy_init(H, rec_c(r), rec_c(l), SeedsH<HYB>::unpack(tl));
+      axpy(H, rec_c(l2), SeedsH<HYB>::unpack(tl2));
     } else {
       leaves<HYB>(st.p + 16, w, rec_c(r), l, H, sd);
       if constexpr (PC == 0) sp = seed_of<0, HYB>(sd, (uint32_t)r.z);
@@ -388,11 +405,13 @@ k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tbase = *tslot;
+  if (tbase != 0) __trap();  // the program's TMEM addresses assume the whole TMEM at column 0
   SeedsH<HYB> sd;
   sd.tq = tbase + ((uint32_t)((warp & 3) * 32) << 16);
   sd.sb = sbase + (uint32_t)(lane * 16);
   sd.gb = nullptr;
   const uint32_t ring = rings + (uint32_t)warp * kHornerRing;
+  const int32_t nops = __ldg(chunk + nchunk);  // records per quadrant copy
   double* mypart = part + (size_t)blockIdx.x * nchunk * 128;
   RingH st;
   const int64_t ntiles = (S + 127) / 128;
@@ -453,7 +472,7 @@ k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __
     for (int ci = cb + warp; ci < ce;) {
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
       const int32_t nr = __ldg(croots + ci);
-      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), ring, lane);
+      st.begin(reinterpret_cast<const int4*>(ops) + (size_t)(warp & 3) * nops + b, (uint32_t)(e - b), ring, lane);
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       for (int32_t k = 0; k < nr; ++k) root<NU, HYB>(st, acc, sd, lane);
 #pragma unroll
@@ -514,6 +533,7 @@ struct HornerEnc {
   uint32_t hot, us, U;
   int nu;
   std::vector<OpH>& out;
+  std::vector<uint8_t> hot_rec;  // record's z is a TMEM column (gets the lane-quadrant bits per copy)
   bool ok = true;
 
   uint32_t cls(uint32_t s) const { return s < hot ? 0u : (s < hot + us ? 1u : 2u); }
@@ -541,6 +561,7 @@ struct HornerEnc {
     for (size_t j = b; j < e; ++j) {
       const Op& l = H.ops[kids[j]];
       out.push_back(OpH{l.c, zof(slot(l)), 0u});
+      hot_rec.push_back(cls(slot(l)) == 0);
     }
   }
   uint32_t leaf_w(const std::vector<size_t>& kids, size_t b, size_t e) {
@@ -564,8 +585,10 @@ struct HornerEnc {
     const Op& o = H.ops[pos];
     const uint32_t z = zof(slot(o));
     const std::vector<size_t> kids = kids_of(pos);
+    const uint8_t zh = cls(slot(o)) == 0;
     if (d == nu) {
       out.push_back(OpH{o.c, z, 0u});
+      hot_rec.push_back(zh);
       return 1;
     }
     if (d == nu - 1) {
@@ -574,6 +597,7 @@ struct HornerEnc {
       do {
         const size_t e = std::min(kids.size(), b + kMaxLeaves);
         out.push_back(OpH{b == 0 ? o.c : 0.0, z, leaf_w(kids, b, e)});
+        hot_rec.push_back(zh);
         emit_leaves(kids, b, e);
         copies++;
         b = e;
@@ -582,6 +606,7 @@ struct HornerEnc {
     }
     const size_t me = out.size();
     out.push_back(OpH{o.c, z, 0u});
+    hot_rec.push_back(zh);
     uint32_t n = 0, nh = 0, ns = 0;
     for (size_t k : kids) count(cls(slot(H.ops[k])), node(k, d + 1), n, nh, ns);
     out[me].w = pack(n, nh, ns);
@@ -602,6 +627,8 @@ struct HornerEnc {
         const size_t e = std::min(kids.size(), bb + kMaxLeaves);
         out.push_back(OpH{first ? a.c : 0.0, zof(sa), leaf_w(kids, bb, e)});
         out.push_back(OpH{0.0, single ? 0u : zof(sb), fl});
+        hot_rec.push_back(cls(sa) == 0);
+        hot_rec.push_back(!single && cls(sb) == 0);
         emit_leaves(kids, bb, e);
         nroots++;
         first = false;
@@ -611,6 +638,8 @@ struct HornerEnc {
       const size_t me = out.size();
       out.push_back(OpH{a.c, zof(sa), 0u});
       out.push_back(OpH{0.0, single ? 0u : zof(sb), fl});
+      hot_rec.push_back(cls(sa) == 0);
+      hot_rec.push_back(!single && cls(sb) == 0);
       uint32_t n = 0, nh = 0, ns = 0;
       for (size_t k : kids) count(cls(slot(H.ops[k])), node(k, 3), n, nh, ns);
       out[me].w = pack(n, nh, ns);
@@ -675,7 +704,17 @@ bool encode_horner(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<OpH
     croots[ci] = nr;
   }
   chunk[nchunk] = (int32_t)out.size();
-  return E.ok && out.size() < (size_t)INT32_MAX;
+  // one copy per TMEM lane quadrant: a TMEM column offset carries the
+  // quadrant's lane bits, so a hot fetch is R2UR + tcgen05.ld with no add
+  const size_t n = out.size();
+  if (E.hot_rec.size() != n) return false;
+  out.resize(4 * n);
+  for (size_t q = 1; q < 4; ++q)
+    for (size_t i = 0; i < n; ++i) {
+      out[q * n + i] = out[i];
+      if (E.hot_rec[i]) out[q * n + i].z += (uint32_t)(q * 32) << 16;
+    }
+  return E.ok && 4 * n < (size_t)INT32_MAX;
 }
 
 template <int NU, bool HYB>

@@ -42,6 +42,8 @@ constexpr uint32_t kMaxLeaves = 30;
 // Re-encodes the plan's DFS program for k2_horner with `hot` TMEM rows and
 // `us` shared-memory rows (slot order: hot, shared, global), chunked like the
 // plan: chunk gets each chunk's first record, croots its number of roots.
+// out holds four copies of the program (one per TMEM lane quadrant: hot
+// records' z carries the quadrant's lane bits), chunk offsets index copy 0.
 // Returns false when a count does not fit its field (another kernel is used).
 bool encode_horner(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<OpH>& out,
                    std::vector<int32_t>& chunk, std::vector<int32_t>& croots);

@@ -566,7 +566,7 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   CK(P->chunk.upload(H.chunk));
   if (k2_mode() == 5 || k2_mode() == 7 || k2_mode() == 9) CK(P->opsQ.upload(reencode_hot(H, dev::kTmemRowsQ)));
   P->opsH_ok = false;
-  if ((k2_mode() == 5 || k2_mode() == 9) && H.max_order <= 4) {
+  if ((k2_mode() == 5 && H.max_order <= 4) || k2_mode() == 9) {
     const int hot = std::min(P->U, (int)kHornerHot);
     P->usH = std::min(P->U - hot, horner_us_max(P->smem_optin));
     std::vector<OpH> oh;
@@ -698,10 +698,11 @@ int k2_warps() {
   return w;
 }
 
-// auto selection (k2_mode 5): four sites per lane pays off where the program
-// is order <= 4 (k2_quad spills deeper) and the sites fill a round of tiles
+// auto selection (k2_mode 5) for order 5-6 (order <= 4 runs k2_horner): four
+// sites per lane when the sites fill a round of tiles (cfg4: 482 ms vs 591 ms
+// for k2_tmem3 at 2e5 sites, profiles/r01)
 bool use_quad(const acedag_plan* P, int64_t S) {
-  return P->host.max_order <= 4 && (S + 127) / 128 >= P->sms - t_sm_reserve;
+  return (S + 127) / 128 >= P->sms - t_sm_reserve;
 }
 
 // tile geometry: 32 sites per CTA, seed rows [Us][32] in smem (U used seeds
@@ -1055,7 +1056,7 @@ bool run_horner(acedag_plan* P, const double2* A, int64_t S, int L, const uint16
 // auto selection (k2_mode 5) prefers k2_horner where k2_quad would run
 bool use_horner(const acedag_plan* P, int64_t S) {
   (void)S;  // every batch size, so a site's value never depends on its batch
-  return P->opsH_ok && P->host.max_order <= 4 && (k2_mode() == 9 || k2_mode() == 5);
+  return P->opsH_ok && ((P->host.max_order <= 4 && k2_mode() == 5) || k2_mode() == 9);
 }
 
 template <int NU> struct QuadF64 {

@@ -743,6 +743,8 @@ cudaError_t launch_horner(int nu, const double2* T, int64_t S, int U, int us, co
     case 2: ACEDAG_H(2);
     case 3: ACEDAG_H(3);
     case 4: ACEDAG_H(4);
+    case 5: ACEDAG_H(5);
+    case 6: ACEDAG_H(6);
     default: return cudaErrorInvalidValue;
   }
 #undef ACEDAG_H

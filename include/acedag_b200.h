@@ -128,14 +128,29 @@ int acedag_plan_info(const acedag_plan* plan, int64_t* recursive_products,
 /* Host-only view of the compiled recursive program (no device needed; used
  * by tests and tooling).  Two-call pattern: pass NULL buffers to get
  * *n_slots / *n_ops, then buffers of that size.  ops receives 16-byte records
- * {double c; uint16 slot_a; uint16 slot_b (0xFFFF: order-1 term); uint32
- * n_children} in DFS preorder; chunk receives warps+1 record offsets;
- * stats = {recursive_products, extra_nodes, naive_products}. */
+ * {double c; uint32 seed-row byte offset (slot * 512); uint16 n_children;
+ * uint16 hot children} in DFS preorder, a root as two records; chunk
+ * receives warps+1 record offsets; stats = {recursive_products,
+ * extra_nodes, naive_products}. */
 int acedag_plan_program(const acedag_graph* g, const int64_t* node_ids,
                         const double* c_re, const double* c_im, int64_t n_coef,
                         int32_t n_out, int32_t warps, uint16_t* slot_label,
                         int64_t* n_slots, void* ops, int64_t* n_ops,
                         int32_t* chunk, int64_t* stats);
+
+/* Host-only view of the k2_horner program (tests and tooling; replaces no
+ * reference function -- it is the device form of evaluator.py:93-142's
+ * work): the recursive program above re-encoded with `hot` TMEM rows and
+ * `us` shared-memory rows (csrc/horner.h: 16-byte records {double c; uint32
+ * z; uint32 w}, children ordered hot / shared / global with their counts in
+ * w), real coefficients, one output.  *n_ops = records of one copy; ops
+ * receives the four TMEM-lane-quadrant copies (4 * *n_ops records), chunk
+ * warps+1 offsets into copy 0, croots the roots per chunk.  Two-call
+ * pattern as acedag_plan_program. */
+int acedag_plan_program_horner(const acedag_graph* g, const int64_t* node_ids,
+                               const double* c_re, int64_t n_coef, int32_t warps,
+                               int32_t hot, int32_t us, void* ops, int64_t* n_ops,
+                               int32_t* chunk, int32_t* croots);
 
 /* Kernels launched by this library since load (all plans and devices). */
 int64_t acedag_launch_count(void);

@@ -43,6 +43,8 @@ SIGNATURES = {
     "acedag_plan_set_coefficients": (C.c_int, [_vp, _i64p, _dp, _dp, C.c_int64, C.c_int32]),
     "acedag_plan_program": (C.c_int, [_vp, _i64p, _dp, _dp, C.c_int64, C.c_int32, C.c_int32, _vp, _i64p,
                                        _vp, _i64p, _i32p, _i64p]),
+    "acedag_plan_program_horner": (C.c_int, [_vp, _i64p, _dp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _vp,
+                                              _i64p, _i32p, _i32p]),
     "acedag_plan_info": (C.c_int, [_vp, _i64p, _i64p, _i64p, _i64p]),
     "acedag_eval": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, _vp]),
     "acedag_eval_kernel_name": (C.c_char_p, [_vp, C.c_int, C.c_int, C.c_int, C.c_int64]),

@@ -633,6 +633,32 @@ int acedag_plan_program(const acedag_graph* h, const int64_t* node_ids, const do
   return ACEDAG_OK;
 }
 
+int acedag_plan_program_horner(const acedag_graph* h, const int64_t* node_ids, const double* c_re,
+                               int64_t n_coef, int32_t warps, int32_t hot, int32_t us, void* ops, int64_t* n_ops,
+                               int32_t* chunk, int32_t* croots) {
+  if (!h || !n_ops || warps < 1 || hot < 0 || hot > (int)kHornerHot || us < 0 || (n_coef && (!node_ids || !c_re)))
+    return fail(ACEDAG_EINVAL, "bad arguments");
+  PlanHost H;
+  std::vector<OpH> out;
+  std::vector<int32_t> ch, cr;
+  try {
+    compile_plan(h->g, node_ids, c_re, nullptr, n_coef, 1, warps, H, (uint32_t)hot);
+    if (!encode_horner(H, (uint32_t)hot, (uint32_t)us, out, ch, cr))
+      return fail(ACEDAG_EUNSUPPORTED, "program does not fit the k2_horner record fields");
+  } catch (const std::domain_error& e) {
+    return fail(ACEDAG_ENOTTARGET, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ACEDAG_ENOMEM, "out of host memory compiling the plan");
+  } catch (const std::exception& e) {
+    return fail(ACEDAG_EINVAL, e.what());
+  }
+  if (ops) std::memcpy(ops, out.data(), out.size() * sizeof(OpH));
+  if (chunk) std::memcpy(chunk, ch.data(), ch.size() * sizeof(int32_t));
+  if (croots) std::memcpy(croots, cr.data(), cr.size() * sizeof(int32_t));
+  *n_ops = (int64_t)(out.size() / 4);
+  return ACEDAG_OK;
+}
+
 int acedag_plan_info(const acedag_plan* P, int64_t* recursive_products, int64_t* extra_nodes,
                      int64_t* naive_products, int64_t* used_seeds) {
   if (!P) return fail(ACEDAG_EINVAL, "plan is NULL");

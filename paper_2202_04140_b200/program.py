@@ -42,3 +42,31 @@ def compile_program(graph, node_ids, values, warps: int = 32) -> dict:
     return {"slot_label": slots[: ns.value], "ops": ops[: no.value], "chunk": chunk,
             "recursive_products": int(stats[0]), "extra_nodes": int(stats[1]),
             "naive_products": int(stats[2])}
+
+
+# k2_horner records (csrc/horner.h): {coefficient, z = class-scaled seed
+# offset, w = nch | nhot << 16 | nsm << 22 (a root's second record: class
+# flags cls_a | cls_b << 2 | single << 4)}
+OPH_DTYPE = np.dtype([("c", "<f8"), ("z", "<u4"), ("w", "<u4")])
+HORNER_HOT, HORNER_MAX_LEAVES = 32, 30
+
+
+def compile_horner(graph, node_ids, values, warps: int = 128, hot: int = HORNER_HOT, us: int = 97) -> dict:
+    """The k2_horner encoding of the recursive program (host only): records
+    of the four TMEM-lane-quadrant copies [4, n], chunk offsets, roots per
+    chunk, and the slot labels of compile_program."""
+    g = as_eval_graph(graph)
+    node_ids = np.ascontiguousarray(np.asarray(node_ids, np.int64).reshape(-1))
+    c_re = np.ascontiguousarray(np.asarray(values, np.float64).reshape(-1))
+    lib = N.lib()
+    no = C.c_int64()
+    args = (g._h, N.ptr(node_ids, C.c_int64), N.ptr(c_re, C.c_double), node_ids.shape[0], warps, hot, us)
+    N.check(lib.acedag_plan_program_horner(*args, None, C.byref(no), None, None))
+    ops = np.empty(4 * max(1, no.value), OPH_DTYPE)
+    chunk = np.empty(warps + 1, np.int32)
+    croots = np.empty(warps, np.int32)
+    N.check(lib.acedag_plan_program_horner(*args, C.c_void_p(ops.ctypes.data), C.byref(no),
+                                           N.ptr(chunk, C.c_int32), N.ptr(croots, C.c_int32)))
+    prog = compile_program(graph, node_ids, c_re, warps)
+    return {"ops": ops[: 4 * no.value].reshape(4, no.value), "chunk": chunk, "croots": croots,
+            "slot_label": prog["slot_label"], "hot": hot, "us": us}

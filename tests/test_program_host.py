@@ -86,3 +86,94 @@ def test_program_rejects_non_target():
     aux_id = g.id_of(((1,), (1,)))
     with pytest.raises(ValueError, match="non-target"):
         compile_program(g, [aux_id], [1.0])
+
+
+# --------------------------------------------------------------- k2_horner
+def simulate_horner(h, A):
+    """Walk copy 0 of the k2_horner program exactly as the kernel does (per
+    chunk: croots roots; children by seed class hot / shared / global from
+    the counts in w; H_u = c_u + sum_children s_q H_q; phi = Re(s_a s_b H))."""
+    from paper_2202_04140_b200.program import HORNER_MAX_LEAVES
+    ops, slots, hot, us = h["ops"][0], h["slot_label"], h["hot"], h["us"]
+    nu = simulate_horner.nu
+    seeds = A[:, slots]  # [S, U]
+
+    def seed(z, cls):
+        if cls == 0:
+            assert z % 16 == 0 and z // 16 < hot
+            return seeds[:, z // 16]
+        assert z % 2048 == 0
+        s = hot + z // 2048 + (us if cls == 2 else 0)
+        assert (cls == 1 and s < hot + us) or (cls == 2 and s >= hot + us)
+        return seeds[:, s]
+
+    def cls_of(j, w):
+        nh, ns = (w >> 16) & 63, w >> 22
+        return 0 if j < nh else (1 if j < nh + ns else 2)
+
+    pos = 0
+
+    def leaves(w, H):
+        nonlocal pos
+        n = w & 0xFFFF
+        assert n <= HORNER_MAX_LEAVES
+        for j in range(n):
+            r = ops[pos]
+            pos += 1
+            assert r["w"] == 0
+            H = H + r["c"] * seed(r["z"], cls_of(j, w))
+        return H
+
+    def children(w, D, Hp):
+        nonlocal pos
+        for j in range(w & 0xFFFF):
+            r = ops[pos]
+            pos += 1
+            H = np.full(A.shape[0], r["c"], complex)
+            H = leaves(r["w"], H) if D == nu - 1 else children(r["w"], D + 1, H)
+            Hp = Hp + seed(r["z"], cls_of(j, w)) * H
+        return Hp
+
+    phi = np.zeros(A.shape[0])
+    chunk, croots = h["chunk"], h["croots"]
+    for ci in range(len(croots)):
+        pos = chunk[ci]
+        for _ in range(croots[ci]):
+            r0, r1 = ops[pos], ops[pos + 1]
+            pos += 2
+            fl = int(r1["w"])
+            H = np.full(A.shape[0], r0["c"], complex)
+            if nu == 3:
+                H = leaves(int(r0["w"]), H)
+            elif nu >= 4:
+                H = children(int(r0["w"]), 3, H)
+            sa = seed(r0["z"], fl & 3)
+            phi = phi + (r0["c"] * sa.real if fl & 16 else (sa * seed(r1["z"], (fl >> 2) & 3) * H).real)
+        assert pos == chunk[ci + 1]
+    return phi
+
+
+@pytest.mark.parametrize("D,nu,hot,us", [(8, 3, 32, 97), (10, 4, 32, 97), (12, 4, 32, 97), (12, 4, 8, 20),
+                                         (12, 3, 4, 6), (6, 2, 32, 0), (9, 5, 16, 40), (14, 4, 32, 97)])
+def test_horner_program_reproduces_oracle(D, nu, hot, us):
+    """The k2_horner encoding (class-sorted children, class-scaled seed
+    offsets, nodes with more than 30 leaves split into copies, per-quadrant
+    copies) evaluated bottom-up on the CPU equals the oracle's model sum;
+    small hot / shared budgets exercise all three seed classes."""
+    from paper_2202_04140_b200.program import compile_horner
+    g = P.build_graph(P.Group.O3, P.DegreeSpec(1, D), nu)
+    c = np.random.default_rng(D + nu).normal(size=len(g.target_ids))
+    h = compile_horner(g, g.target_ids, c, warps=32, hot=hot, us=us)
+    ops = h["ops"]
+    # copies differ only in the lane-quadrant bits of TMEM (class 0) offsets
+    for q in range(1, 4):
+        d = ops[q]["z"].astype(np.int64) - ops[0]["z"].astype(np.int64)
+        assert set(np.unique(d)) <= {0, q << 21}
+        assert np.array_equal(ops[q]["c"], ops[0]["c"]) and np.array_equal(ops[q]["w"], ops[0]["w"])
+    A = seeded_A(5, g.num_seeds, 11)
+    simulate_horner.nu = max(2, g.max_order)
+    phi = simulate_horner(h, A)
+    re, im = O.evaluate_nodes(g.parents[:, 0], g.parents[:, 1], A)
+    ref, _ = O.model_sum(re, im, g.target_ids, c)
+    ok, worst = phi_gate(phi, ref, O.energy_scale(re, g.target_ids, c))
+    assert ok, worst

@@ -299,10 +299,13 @@ struct acedag_plan {
   DevBuf<int4> tri;        // (n, l, m >= 0) triples the used labels need
   DevBuf<Op> ops;
   DevBuf<Op> opsQ;         // k2_quad: hot counts for its 32 TMEM slots
-  DevBuf<OpH> opsH;        // k2_horner encoding (encode_horner), if it fits
-  DevBuf<int32_t> crootsH, chunkH;
-  bool opsH_ok = false;
-  int usH = 0;             // k2_horner shared-memory rows
+  // k2_horner encodings (encode_horner) for fp64 [0] and the fp32 mode [1]
+  struct HornerProg {
+    DevBuf<OpH> ops;
+    DevBuf<int32_t> croots, chunk;
+    bool ok = false;
+    int us = 0;  // shared-memory rows
+  } hp[2];
   DevBuf<Op> ops4;         // k2_tmem4 encoding (encode_ops4), if it fits
   DevBuf<int32_t> croots;  // roots per chunk
   bool ops4_ok = false;
@@ -565,19 +568,6 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   CK(P->ops.upload(H.ops));
   CK(P->chunk.upload(H.chunk));
   if (k2_mode() == 5 || k2_mode() == 7 || k2_mode() == 9) CK(P->opsQ.upload(reencode_hot(H, dev::kTmemRowsQ)));
-  P->opsH_ok = false;
-  if ((k2_mode() == 5 && H.max_order <= 4) || k2_mode() == 9) {
-    const int hot = std::min(P->U, (int)kHornerHot);
-    P->usH = std::min(P->U - hot, horner_us_max(P->smem_optin));
-    std::vector<OpH> oh;
-    std::vector<int32_t> ch, cr;
-    P->opsH_ok = encode_horner(H, (uint32_t)hot, (uint32_t)P->usH, oh, ch, cr);
-    if (P->opsH_ok) {
-      CK(P->opsH.upload(oh));
-      CK(P->chunkH.upload(ch));
-      CK(P->crootsH.upload(cr));
-    }
-  }
   if (k2_mode() == 6) {
     const int rows = P->U + 1, cold = std::max(0, rows - (int)dev::kTmemRows2);
     std::vector<Op> o4;
@@ -586,6 +576,22 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
     if (P->ops4_ok) {
       CK(P->ops4.upload(o4));
       CK(P->croots.upload(cr));
+    }
+  }
+  for (int f = 0; f < 2; ++f) {
+    acedag_plan::HornerProg& hp = P->hp[f];
+    hp.ok = false;
+    if ((k2_mode() == 5 && H.max_order <= 4) || (k2_mode() == 9 && (f == 0 || H.max_order <= 4))) {
+      const int hot = std::min(P->U, horner_hot_rows(f == 1));
+      hp.us = std::min(P->U - hot, horner_us_max(P->smem_optin, f == 1));
+      std::vector<OpH> oh;
+      std::vector<int32_t> ch, cr;
+      hp.ok = encode_horner(H, f == 1, (uint32_t)hot, (uint32_t)hp.us, oh, ch, cr);
+      if (hp.ok) {
+        CK(hp.ops.upload(oh));
+        CK(hp.chunk.upload(ch));
+        CK(hp.croots.upload(cr));
+      }
     }
   }
   {
@@ -643,7 +649,7 @@ int acedag_plan_program_horner(const acedag_graph* h, const int64_t* node_ids, c
   std::vector<int32_t> ch, cr;
   try {
     compile_plan(h->g, node_ids, c_re, nullptr, n_coef, 1, warps, H, (uint32_t)hot);
-    if (!encode_horner(H, (uint32_t)hot, (uint32_t)us, out, ch, cr))
+    if (!encode_horner(H, false, (uint32_t)hot, (uint32_t)us, out, ch, cr))
       return fail(ACEDAG_EUNSUPPORTED, "program does not fit the k2_horner record fields");
   } catch (const std::domain_error& e) {
     return fail(ACEDAG_ENOTTARGET, e.what());
@@ -907,8 +913,8 @@ bool use_tiled();
 
 // the tile-major seed copy (k_tile_seeds<TS>) for an eval_impl input, or
 // false when the input layout is not one the plan knows
-template <int TS>
-bool tile_seeds(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
+template <int TS, typename V = double2>
+bool tile_seeds(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* slot_label,
                 acedag_plan::Workspace* ws, cudaStream_t st, cudaError_t& e) {
   e = cudaSuccess;
   const int32_t* cols = nullptr;
@@ -924,14 +930,15 @@ bool tile_seeds(acedag_plan* P, const double2* A, int64_t S, int L, const uint16
   const int64_t ntiles = (S + TS - 1) / TS;
   e = ws->tiles.alloc((size_t)ntiles * (P->U + 1) * TS);
   if (e != cudaSuccess) return true;
-  constexpr size_t tsm = 32 * (TS + 1) * 16;
+  constexpr size_t tsm = 32 * (TS + 1) * sizeof(V);
   static bool attr = false;
   if (!attr) {
-    e = cudaFuncSetAttribute(dev::k_tile_seeds<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    e = cudaFuncSetAttribute(dev::k_tile_seeds<TS, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     if (e != cudaSuccess) return true;
     attr = true;
   }
-  dev::k_tile_seeds<TS><<<(unsigned)ntiles, 512, tsm, st>>>(A, S, L, cols, slots, P->U, ws->tiles.p); note_launch();
+  dev::k_tile_seeds<TS, V><<<(unsigned)ntiles, 512, tsm, st>>>(A, S, L, cols, slots, P->U,
+                                                                   reinterpret_cast<V*>(ws->tiles.p)); note_launch();
   e = cudaGetLastError();
   return true;
 }
@@ -1047,11 +1054,15 @@ cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, co
   return cudaGetLastError();
 }
 
-// k2_horner on the tile-major seed table; false (nothing launched) when the
-// input layout is not one tile_seeds knows
-bool run_horner(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label, double* out,
+// k2_horner on the tile-major seed table (V: double2, or float2 for the fp32
+// mode); false (nothing launched) when the input layout is not one
+// tile_seeds knows
+template <typename V>
+bool run_horner(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* slot_label, double* out,
                 Launch& lc, cudaStream_t st, cudaError_t& e) {
-  if (!tile_seeds<128>(P, A, S, L, slot_label, lc.ws, st, e)) return false;
+  constexpr bool f32 = sizeof(V) == 8;
+  const acedag_plan::HornerProg& hp = P->hp[f32 ? 1 : 0];
+  if (!tile_seeds<128, V>(P, A, S, L, slot_label, lc.ws, st, e)) return false;
   if (e != cudaSuccess) return true;
   mark_prep(st);
   const int64_t ntiles = (S + 127) / 128;
@@ -1067,7 +1078,7 @@ bool run_horner(acedag_plan* P, const double2* A, int64_t S, int L, const uint16
     e = lc.ws->tail.alloc((size_t)(ntiles - full) * nch * 128);
     if (e != cudaSuccess) return true;
   }
-  e = launch_horner(P->host.max_order, lc.ws->tiles.p, S, P->U, P->usH, P->opsH.p, P->chunkH.p, P->crootsH.p, nch,
+  e = launch_horner(P->host.max_order, f32, lc.ws->tiles.p, S, P->U, hp.us, hp.ops.p, hp.chunk.p, hp.croots.p, nch,
                     out, lc.ws->part.p, full, parts, lc.ws->tail.p, grid, st);
   note_launch();
   mark_main(st);
@@ -1079,10 +1090,12 @@ bool run_horner(acedag_plan* P, const double2* A, int64_t S, int L, const uint16
   return true;
 }
 
-// auto selection (k2_mode 5) prefers k2_horner where k2_quad would run
-bool use_horner(const acedag_plan* P, int64_t S) {
-  (void)S;  // every batch size, so a site's value never depends on its batch
-  return P->opsH_ok && ((P->host.max_order <= 4 && k2_mode() == 5) || k2_mode() == 9);
+// auto selection (k2_mode 5) prefers k2_horner for order <= 4 (every batch
+// size, so a site's value never depends on its batch); f32: the fp32 mode
+bool use_horner(const acedag_plan* P, int64_t S, bool f32 = false) {
+  (void)S;
+  const acedag_plan::HornerProg& hp = P->hp[f32 ? 1 : 0];
+  return hp.ok && ((P->host.max_order <= 4 && k2_mode() == 5) || k2_mode() == 9);
 }
 
 template <int NU> struct QuadF64 {
@@ -1339,7 +1352,9 @@ int eval_body(acedag_plan* P, int method, int prec, int out_kind, const void* A,
   if (method == ACEDAG_METHOD_RECURSIVE) {
     if (prec == ACEDAG_PREC_F32) {
       if (!fast) return fail(ACEDAG_EUNSUPPORTED, "fp32 mode supports real coefficients, one real output");
-      if (k2_spl() == 2) {
+      if (use_horner(P, S, true) && run_horner(P, (const float2*)A, S, L, slot_label, (double*)out, lc, st, e)) {
+        if (e != cudaSuccess) return cuda_fail(e, "k2_horner (fp32)");
+      } else if (k2_spl() == 2) {
         int rc = plan_launch(P, S, sizeof(float2), k2_warps() * 1024, k2_warps(), lc, 64);
         if (rc) return rc;
         e = by_order<Fast2F32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
@@ -1570,7 +1585,8 @@ const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, 
   const PlanHost& H = P->host;
   const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
   if (method == ACEDAG_METHOD_NAIVE) return "k3_naive";
-  if (prec == ACEDAG_PREC_F32) return k2_spl() == 2 ? "k2_fast2 (fp32)" : "k2_fast (fp32)";
+  if (prec == ACEDAG_PREC_F32)
+    return use_horner(P, S, true) ? "k2_horner (fp32)" : (k2_spl() == 2 ? "k2_fast2 (fp32)" : "k2_fast (fp32)");
   if (fast) {
     switch (k2_mode()) {
       case 8: return "k2_tmem3";

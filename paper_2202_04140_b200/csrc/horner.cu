@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 #include <vector>
 
@@ -30,17 +31,44 @@ namespace hdev {
 
 extern __shared__ __align__(16) unsigned char h_smem[];
 
-struct C4 {
-  double2 v[4];
+// precision traits: a TMEM row holds the four sites of a lane (16 columns
+// of c128, 8 of c64); a shared/global row holds the tile's 128 sites
+template <typename T> struct HTr;
+template <> struct HTr<double> {
+  using V = double2;
+  static constexpr int kCols = 16;
+  static constexpr uint32_t kRow = 2048;
 };
+template <> struct HTr<float> {
+  using V = float2;
+  static constexpr int kCols = 8;
+  static constexpr uint32_t kRow = 1024;
+};
+
+template <typename T>
+struct C4 {
+  typename HTr<T>::V v[4];
+};
+
+__device__ __forceinline__ double fmaT(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float fmaT(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double mulT(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mulT(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double2 mk2(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
 
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
+__device__ __forceinline__ float2 ld_stream(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
 
-__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tmem_ld(uint32_t addr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
       "%15}, [%16];\n"
@@ -48,11 +76,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&r)[16]) {
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(addr));
 }
+__device__ __forceinline__ void tmem_ld(uint32_t addr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void tmem_st8(uint32_t addr, double2 a, double2 b) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(addr),
-               "r"(__double2loint(a.x)), "r"(__double2hiint(a.x)), "r"(__double2loint(a.y)), "r"(__double2hiint(a.y)),
-               "r"(__double2loint(b.x)), "r"(__double2hiint(b.x)), "r"(__double2loint(b.y)), "r"(__double2hiint(b.y)));
+__device__ __forceinline__ void tmem_st8(uint32_t addr, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t a4,
+                                         uint32_t a5, uint32_t a6, uint32_t a7) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(addr), "r"(a0),
+               "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7));
+}
+// one TMEM row: the lane's four sites
+__device__ __forceinline__ void tmem_st_row(uint32_t addr, const double2 (&v)[4]) {
+  tmem_st8(addr, __double2loint(v[0].x), __double2hiint(v[0].x), __double2loint(v[0].y), __double2hiint(v[0].y),
+           __double2loint(v[1].x), __double2hiint(v[1].x), __double2loint(v[1].y), __double2hiint(v[1].y));
+  tmem_st8(addr + 8, __double2loint(v[2].x), __double2hiint(v[2].x), __double2loint(v[2].y), __double2hiint(v[2].y),
+           __double2loint(v[3].x), __double2hiint(v[3].x), __double2loint(v[3].y), __double2hiint(v[3].y));
+}
+__device__ __forceinline__ void tmem_st_row(uint32_t addr, const float2 (&v)[4]) {
+  tmem_st8(addr, __float_as_uint(v[0].x), __float_as_uint(v[0].y), __float_as_uint(v[1].x), __float_as_uint(v[1].y),
+           __float_as_uint(v[2].x), __float_as_uint(v[2].y), __float_as_uint(v[3].x), __float_as_uint(v[3].y));
 }
 
 __device__ __forceinline__ int4 lds128(uint32_t a) {
@@ -60,7 +104,12 @@ __device__ __forceinline__ int4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
   return r;
 }
-__device__ __forceinline__ double rec_c(int4 r) { return __hiloint2double(r.y, r.x); }
+// a record's coefficient: fp64, or (fp32 programs) the float in its low word
+template <typename T>
+__device__ __forceinline__ T rec_c(int4 r) {
+  if constexpr (sizeof(T) == 8) return __hiloint2double(r.y, r.x);
+  else return __int_as_float(r.x);
+}
 
 // ------------------------------------------------------------ program ring
 struct RingH {
@@ -121,37 +170,49 @@ struct RingH {
 };
 
 // ------------------------------------------------------------------- seeds
-template <bool HYB>
+template <typename T, bool HYB>
 struct SeedsH {
+  using V = typename HTr<T>::V;
+  static constexpr int kC = HTr<T>::kCols;
+  static constexpr uint32_t kQ = HTr<T>::kRow / 4;  // bytes between a lane's four sites in a row
+  using Tm = uint32_t[kC];
   uint32_t tq;     // TMEM address of this warp's lane quadrant, column 0
-  uint32_t sb;     // shared address of cold row 0 + lane * 16
-  const char* gb;  // global tail row 0 of this tile + lane * 16
+  uint32_t sb;     // shared address of cold row 0 + lane * sizeof(V)
+  const char* gb;  // global tail row 0 of this tile + lane * sizeof(V)
   // z: TMEM address of the row in this warp's lane quadrant (the program
   // copy of the quadrant carries the lane bits; the allocation base is 0)
-  __device__ __forceinline__ void hot(uint32_t z, uint32_t (&t)[16]) const { tmem_ld16(z, t); }
-  __device__ __forceinline__ static C4 unpack(const uint32_t (&t)[16]) {
-    C4 s;
+  __device__ __forceinline__ void hot(uint32_t z, Tm& t) const { tmem_ld(z, t); }
+  __device__ __forceinline__ static C4<T> unpack(const Tm& t) {
+    C4<T> s;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      s.v[k] = make_double2(__hiloint2double(t[4 * k + 1], t[4 * k]), __hiloint2double(t[4 * k + 3], t[4 * k + 2]));
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (sizeof(T) == 8)
+        s.v[k] = make_double2(__hiloint2double(t[4 * k + 1], t[4 * k]), __hiloint2double(t[4 * k + 3], t[4 * k + 2]));
+      else
+        s.v[k] = make_float2(__uint_as_float(t[2 * k]), __uint_as_float(t[2 * k + 1]));
+    }
     return s;
   }
-  __device__ __forceinline__ C4 sm(uint32_t z) const {
-    C4 s;
+  __device__ __forceinline__ C4<T> sm(uint32_t z) const {
+    C4<T> s;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(s.v[k].x), "=d"(s.v[k].y) : "r"(sb + z + k * 512));
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (sizeof(T) == 8)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(s.v[k].x), "=d"(s.v[k].y) : "r"(sb + z + k * kQ));
+      else
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(s.v[k].x), "=f"(s.v[k].y) : "r"(sb + z + k * kQ));
+    }
     return s;
   }
-  __device__ __forceinline__ C4 gl(uint32_t z) const {
-    C4 s;
+  __device__ __forceinline__ C4<T> gl(uint32_t z) const {
+    C4<T> s;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) s.v[k] = __ldg(reinterpret_cast<const double2*>(gb + z + k * 512));
+    for (int k = 0; k < 4; ++k) s.v[k] = __ldg(reinterpret_cast<const V*>(gb + z + k * kQ));
     return s;
   }
-  __device__ __forceinline__ C4 get(uint32_t z, uint32_t cls) const {
+  __device__ __forceinline__ C4<T> get(uint32_t z, uint32_t cls) const {
     if (cls == 0) {
-      uint32_t t[16];
+      Tm t;
       hot(z, t);
       tmem_wait_ld();
       return unpack(t);
@@ -161,41 +222,54 @@ struct SeedsH {
   }
 };
 
-__device__ __forceinline__ void init_h(C4& H, double c) {
+template <typename T>
+__device__ __forceinline__ void init_h(C4<T>& H, T c) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) H.v[k] = make_double2(c, 0.0);
+  for (int k = 0; k < 4; ++k) H.v[k] = mk2(c, T(0));
 }
 // H += c s
-__device__ __forceinline__ void axpy(C4& H, double c, const C4& s) {
+template <typename T>
+__device__ __forceinline__ void axpy(C4<T>& H, T c, const C4<T>& s) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    H.v[k].x = __fma_rn(c, s.v[k].x, H.v[k].x);
-    H.v[k].y = __fma_rn(c, s.v[k].y, H.v[k].y);
+    H.v[k].x = fmaT(c, s.v[k].x, H.v[k].x);
+    H.v[k].y = fmaT(c, s.v[k].y, H.v[k].y);
+  }
+}
+// H = c + c_l s (the accumulator's first term folded into its FMAs)
+template <typename T>
+__device__ __forceinline__ void axpy_init(C4<T>& H, T c, T cl, const C4<T>& s) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    H.v[k].x = fmaT(cl, s.v[k].x, c);
+    H.v[k].y = mulT(cl, s.v[k].y);
   }
 }
 // Hp += s H
-__device__ __forceinline__ void cmac(C4& Hp, const C4& s, const C4& H) {
+template <typename T>
+__device__ __forceinline__ void cmac(C4<T>& Hp, const C4<T>& s, const C4<T>& H) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    Hp.v[k].x = __fma_rn(s.v[k].x, H.v[k].x, Hp.v[k].x);
-    Hp.v[k].y = __fma_rn(s.v[k].x, H.v[k].y, Hp.v[k].y);
-    Hp.v[k].x = __fma_rn(-s.v[k].y, H.v[k].y, Hp.v[k].x);
-    Hp.v[k].y = __fma_rn(s.v[k].y, H.v[k].x, Hp.v[k].y);
+    Hp.v[k].x = fmaT(s.v[k].x, H.v[k].x, Hp.v[k].x);
+    Hp.v[k].y = fmaT(s.v[k].x, H.v[k].y, Hp.v[k].y);
+    Hp.v[k].x = fmaT(-s.v[k].y, H.v[k].y, Hp.v[k].x);
+    Hp.v[k].y = fmaT(s.v[k].y, H.v[k].x, Hp.v[k].y);
   }
 }
 
-__device__ __forceinline__ uint32_t w_nch(uint32_t w) { return w & 0xFFFFu; }
-__device__ __forceinline__ uint32_t w_nhot(uint32_t w) { return (w >> 16) & 63u; }
+__device__ __forceinline__ uint32_t w_nch(uint32_t w) { return w & 0x7FFFu; }
+__device__ __forceinline__ uint32_t w_nhot(uint32_t w) { return (w >> 15) & 127u; }
 __device__ __forceinline__ uint32_t w_nsm(uint32_t w) { return w >> 22; }
+constexpr uint32_t kOneHot = 1u | 1u << 15, kTwoHot = 2u | 2u << 15;
 
 // ---------------------------------------------------------------- program walk
-template <uint32_t PC, bool HYB>
-__device__ __forceinline__ C4 seed_of(const SeedsH<HYB>& sd, uint32_t z) {
+template <uint32_t PC, typename T, bool HYB>
+__device__ __forceinline__ C4<T> seed_of(const SeedsH<T, HYB>& sd, uint32_t z) {
   if constexpr (PC == 0) {
-    uint32_t t[16];
+    typename SeedsH<T, HYB>::Tm t;
     sd.hot(z, t);
     tmem_wait_ld();
-    return SeedsH<HYB>::unpack(t);
+    return SeedsH<T, HYB>::unpack(t);
   } else if constexpr (PC == 1) {
     return sd.sm(z);
   } else {
@@ -203,31 +277,22 @@ __device__ __forceinline__ C4 seed_of(const SeedsH<HYB>& sd, uint32_t z) {
   }
 }
 
-// H = c + c_l s (the accumulator's first term folded into its FMAs)
-__device__ __forceinline__ void axpy_init(C4& H, double c, double cl, const C4& s) {
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    H.v[k].x = __fma_rn(cl, s.v[k].x, c);
-    H.v[k].y = __dmul_rn(cl, s.v[k].y);
-  }
-}
-
 // hot leaves [q, qh) two per TMEM round trip
-template <bool HYB>
-__device__ __forceinline__ void hot_leaves(uint32_t q, uint32_t qh, C4& H, const SeedsH<HYB>& sd) {
+template <typename T, bool HYB>
+__device__ __forceinline__ void hot_leaves(uint32_t q, uint32_t qh, C4<T>& H, const SeedsH<T, HYB>& sd) {
 #pragma unroll 1
   for (; q + 16 < qh; q += 32) {
     const int4 r0 = lds128(q), r1 = lds128(q + 16);
-    uint32_t t0[16], t1[16];
+    typename SeedsH<T, HYB>::Tm t0, t1;
     sd.hot((uint32_t)r0.z, t0);
     sd.hot((uint32_t)r1.z, t1);
     tmem_wait_ld();
-    axpy(H, rec_c(r0), SeedsH<HYB>::unpack(t0));
-    axpy(H, rec_c(r1), SeedsH<HYB>::unpack(t1));
+    axpy(H, rec_c<T>(r0), SeedsH<T, HYB>::unpack(t0));
+    axpy(H, rec_c<T>(r1), SeedsH<T, HYB>::unpack(t1));
   }
   if (q < qh) {
     const int4 r = lds128(q);
-    axpy(H, rec_c(r), seed_of<0, HYB>(sd, (uint32_t)r.z));
+    axpy(H, rec_c<T>(r), seed_of<0>(sd, (uint32_t)r.z));
   }
 }
 
@@ -236,17 +301,17 @@ __device__ __forceinline__ void hot_leaves(uint32_t q, uint32_t qh, C4& H, const
 // kMaxLeaves, so they lie in the checked ring window.  The first leaf's FMA
 // carries c; a node whose leaves are all hot (the usual case) skips the
 // other loops.
-template <bool HYB>
-__device__ __forceinline__ void leaves(uint32_t q, uint32_t w, double c, int4 l, C4& H, const SeedsH<HYB>& sd) {
+template <typename T, bool HYB>
+__device__ __forceinline__ void leaves(uint32_t q, uint32_t w, T c, int4 l, C4<T>& H, const SeedsH<T, HYB>& sd) {
   const uint32_t nh = w_nhot(w), ns = w_nsm(w), n = w_nch(w);
   const uint32_t qh = q + nh * 16, qs = qh + ns * 16, qe = q + n * 16;
   if (nh) {
-    axpy_init(H, c, rec_c(l), seed_of<0, HYB>(sd, (uint32_t)l.z));
-    hot_leaves<HYB>(q + 16, qh, H, sd);
+    axpy_init(H, c, rec_c<T>(l), seed_of<0>(sd, (uint32_t)l.z));
+    hot_leaves(q + 16, qh, H, sd);
     if (nh == n) return;
     q = qh;
   } else if (n) {
-    axpy_init(H, c, rec_c(l), ns ? sd.sm((uint32_t)l.z) : sd.gl((uint32_t)l.z));
+    axpy_init(H, c, rec_c<T>(l), ns ? sd.sm((uint32_t)l.z) : sd.gl((uint32_t)l.z));
     q += 16;
   } else {
     init_h(H, c);
@@ -255,146 +320,158 @@ __device__ __forceinline__ void leaves(uint32_t q, uint32_t w, double c, int4 l,
 #pragma unroll 1
   for (; q < qs; q += 16) {
     const int4 r = lds128(q);
-    axpy(H, rec_c(r), sd.sm((uint32_t)r.z));
+    axpy(H, rec_c<T>(r), sd.sm((uint32_t)r.z));
   }
   if constexpr (HYB) {
 #pragma unroll 1
     for (; q < qe; q += 16) {
       const int4 r = lds128(q);
-      axpy(H, rec_c(r), sd.gl((uint32_t)r.z));
+      axpy(H, rec_c<T>(r), sd.gl((uint32_t)r.z));
     }
   }
 }
 
 // n sibling nodes of order NU-1 whose seeds are of class PC; each adds
 // s * (c + sum_leaves c_l s_l) to Hp.  The node record and the one after it
-// (its first leaf) are read together; for the commonest shape (one hot
-// leaf) the leaf seed and a hot node seed are fetched by one TMEM round trip.
-template <uint32_t PC, bool HYB>
-__device__ __forceinline__ void parents(RingH& st, uint32_t n, C4& Hp, const SeedsH<HYB>& sd, int lane) {
+// (its first leaf) are read together; for the commonest shapes (one or two
+// hot leaves) the leaf seeds and a hot node seed share one TMEM round trip.
+template <uint32_t PC, typename T, bool HYB>
+__device__ __forceinline__ void parents(RingH& st, uint32_t n, C4<T>& Hp, const SeedsH<T, HYB>& sd, int lane) {
+  using SD = SeedsH<T, HYB>;
 #pragma unroll 1
   for (uint32_t j = 0; j < n; ++j) {
     const int4 r = st.at(0), l = st.at(1);
     const uint32_t w = (uint32_t)r.w;
-    C4 H, sp;
-    if (w == (1u | 1u << 16)) {  // one hot leaf (the commonest shape)
-      uint32_t tl[16];
+    C4<T> H, sp;
+    if (w == kOneHot) {
+      typename SD::Tm tl;
       sd.hot((uint32_t)l.z, tl);
       if constexpr (PC == 0) {
-        uint32_t tp[16];
+        typename SD::Tm tp;
         sd.hot((uint32_t)r.z, tp);
         tmem_wait_ld();
-        sp = SeedsH<HYB>::unpack(tp);
+        sp = SD::unpack(tp);
       } else {
         tmem_wait_ld();
       }
-      axpy_init(H, rec_c(r), rec_c(l), SeedsH<HYB>::unpack(tl));
-    } else if (w == (2u | 2u << 16)) {  // two hot leaves (the next commonest)
+      axpy_init(H, rec_c<T>(r), rec_c<T>(l), SD::unpack(tl));
+    } else if (w == kTwoHot) {
       const int4 l2 = st.at(2);
-      uint32_t tl[16], tl2[16];
+      typename SD::Tm tl, tl2;
       sd.hot((uint32_t)l.z, tl);
       sd.hot((uint32_t)l2.z, tl2);
       if constexpr (PC == 0) {
-        uint32_t tp[16];
+        typename SD::Tm tp;
         sd.hot((uint32_t)r.z, tp);
         tmem_wait_ld();
-        sp = SeedsH<HYB>::unpack(tp);
+        sp = SD::unpack(tp);
       } else {
         tmem_wait_ld();
       }
-      axpy_init(H, rec_c(r), rec_c(l), SeedsH<HYB>::unpack(tl));
-      axpy(H, rec_c(l2), SeedsH<HYB>::unpack(tl2));
+      axpy_init(H, rec_c<T>(r), rec_c<T>(l), SD::unpack(tl));
+      axpy(H, rec_c<T>(l2), SD::unpack(tl2));
     } else {
-      leaves<HYB>(st.p + 16, w, rec_c(r), l, H, sd);
-      if constexpr (PC == 0) sp = seed_of<0, HYB>(sd, (uint32_t)r.z);
+      leaves(st.p + 16, w, rec_c<T>(r), l, H, sd);
+      if constexpr (PC == 0) sp = seed_of<0>(sd, (uint32_t)r.z);
     }
-    if constexpr (PC != 0) sp = seed_of<PC, HYB>(sd, (uint32_t)r.z);
+    if constexpr (PC != 0) sp = seed_of<PC>(sd, (uint32_t)r.z);
     cmac(Hp, sp, H);
     st.p += 16 * (1 + w_nch(w));
     st.check(lane);
   }
 }
 
-template <int D, int NU, bool HYB>
-__device__ __forceinline__ void children(RingH& st, uint32_t w, C4& Hp, const SeedsH<HYB>& sd, int lane);
+template <int D, int NU, typename T, bool HYB>
+__device__ __forceinline__ void children(RingH& st, uint32_t w, C4<T>& Hp, const SeedsH<T, HYB>& sd, int lane);
 
 // n sibling nodes of order D < NU-1 with seeds of class PC
-template <int D, int NU, uint32_t PC, bool HYB>
-__device__ __forceinline__ void inner(RingH& st, uint32_t n, C4& Hp, const SeedsH<HYB>& sd, int lane) {
+template <int D, int NU, uint32_t PC, typename T, bool HYB>
+__device__ __forceinline__ void inner(RingH& st, uint32_t n, C4<T>& Hp, const SeedsH<T, HYB>& sd, int lane) {
 #pragma unroll 1
   for (uint32_t j = 0; j < n; ++j) {
     const int4 r = st.at(0);
     st.p += 16;
     st.check(lane);
-    C4 H;
-    init_h(H, rec_c(r));
-    children<D + 1, NU, HYB>(st, (uint32_t)r.w, H, sd, lane);
-    cmac(Hp, seed_of<PC, HYB>(sd, (uint32_t)r.z), H);
+    C4<T> H;
+    init_h(H, rec_c<T>(r));
+    children<D + 1, NU>(st, (uint32_t)r.w, H, sd, lane);
+    cmac(Hp, seed_of<PC>(sd, (uint32_t)r.z), H);
   }
 }
 
 // the children (order D) of a node whose accumulator is Hp, by seed class;
 // the ring was checked right before the first child record
-template <int D, int NU, bool HYB>
-__device__ __forceinline__ void children(RingH& st, uint32_t w, C4& Hp, const SeedsH<HYB>& sd, int lane) {
+template <int D, int NU, typename T, bool HYB>
+__device__ __forceinline__ void children(RingH& st, uint32_t w, C4<T>& Hp, const SeedsH<T, HYB>& sd, int lane) {
   const uint32_t nh = w_nhot(w), ns = w_nsm(w), ng = w_nch(w) - nh - ns;
   if constexpr (D == NU - 1) {
-    parents<0, HYB>(st, nh, Hp, sd, lane);
-    parents<1, HYB>(st, ns, Hp, sd, lane);
-    if (HYB) parents<2, HYB>(st, ng, Hp, sd, lane);
+    parents<0>(st, nh, Hp, sd, lane);
+    parents<1>(st, ns, Hp, sd, lane);
+    if (HYB) parents<2>(st, ng, Hp, sd, lane);
   } else if constexpr (D < NU - 1) {
-    inner<D, NU, 0, HYB>(st, nh, Hp, sd, lane);
-    inner<D, NU, 1, HYB>(st, ns, Hp, sd, lane);
-    if (HYB) inner<D, NU, 2, HYB>(st, ng, Hp, sd, lane);
+    inner<D, NU, 0>(st, nh, Hp, sd, lane);
+    inner<D, NU, 1>(st, ns, Hp, sd, lane);
+    if (HYB) inner<D, NU, 2>(st, ng, Hp, sd, lane);
   }
 }
 
-template <int NU, bool HYB>
-__device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<HYB>& sd, int lane) {
+template <int NU, typename T, bool HYB>
+__device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<T, HYB>& sd, int lane) {
   const int4 r0 = st.at(0), r1 = st.at(1);
-  const double c = rec_c(r0);
+  const T c = rec_c<T>(r0);
   const uint32_t fl = (uint32_t)r1.w;
-  C4 H;
+  C4<T> H;
   if constexpr (NU == 3) {
-    leaves<HYB>(st.p + 32, (uint32_t)r0.w, c, st.at(2), H, sd);
+    leaves(st.p + 32, (uint32_t)r0.w, c, st.at(2), H, sd);
     st.p += 16 * (2 + w_nch((uint32_t)r0.w));
     st.check(lane);
   } else {
     init_h(H, c);
     st.p += 32;
     st.check(lane);
-    if constexpr (NU >= 4) children<3, NU, HYB>(st, (uint32_t)r0.w, H, sd, lane);
+    if constexpr (NU >= 4) children<3, NU>(st, (uint32_t)r0.w, H, sd, lane);
   }
-  const C4 sa = sd.get((uint32_t)r0.z, fl & 3u);
+  const C4<T> sa = sd.get((uint32_t)r0.z, fl & 3u);
   if (fl & 16u) {  // order-1 coefficient: c Re(s_a)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc[k] = __fma_rn(c, sa.v[k].x, acc[k]);
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (sizeof(T) == 8) acc[k] = __fma_rn(c, sa.v[k].x, acc[k]);
+      else acc[k] += (double)(c * sa.v[k].x);
+    }
   } else {
-    const C4 sb = sd.get((uint32_t)r1.z, (fl >> 2) & 3u);
+    const C4<T> sb = sd.get((uint32_t)r1.z, (fl >> 2) & 3u);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const double abx = __fma_rn(sa.v[k].x, sb.v[k].x, -__dmul_rn(sa.v[k].y, sb.v[k].y));
-      const double aby = __fma_rn(sa.v[k].x, sb.v[k].y, __dmul_rn(sa.v[k].y, sb.v[k].x));
-      acc[k] = __fma_rn(abx, H.v[k].x, acc[k]);
-      acc[k] = __fma_rn(-aby, H.v[k].y, acc[k]);
+      const T abx = fmaT(sa.v[k].x, sb.v[k].x, -mulT(sa.v[k].y, sb.v[k].y));
+      const T aby = fmaT(sa.v[k].x, sb.v[k].y, mulT(sa.v[k].y, sb.v[k].x));
+      if constexpr (sizeof(T) == 8) {
+        acc[k] = __fma_rn(abx, H.v[k].x, acc[k]);
+        acc[k] = __fma_rn(-aby, H.v[k].y, acc[k]);
+      } else {  // the site's sum over roots in fp64
+        acc[k] += (double)fmaT(abx, H.v[k].x, -mulT(aby, H.v[k].y));
+      }
     }
   }
 }
 
-// T: tile-major seed table [ntiles][U + 1][128] c128
-template <int NU, bool HYB, int W>
+// Tab: tile-major seed table [ntiles][U + 1][128] (c128 or c64)
+template <int NU, typename T, bool HYB, int W>
 __global__ void __launch_bounds__(W * 32, 1)
-k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __restrict__ ops,
+k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, const OpH* __restrict__ ops,
           const int32_t* __restrict__ chunk, const int32_t* __restrict__ croots, int nchunk,
           double* __restrict__ out, double* __restrict__ part, int64_t full_tiles, int tail_parts,
           double* __restrict__ tailbuf) {
+  using V = typename HTr<T>::V;
+  constexpr int kC = HTr<T>::kCols;
+  constexpr uint32_t kRow = HTr<T>::kRow;
+  constexpr int kHot = 512 / kC;
   unsigned char* smem = h_smem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rows = U + 1;  // table rows (row U: the constant ONE, unused here)
-  const int hot = U < (int)kHornerHot ? U : (int)kHornerHot;
+  const int hot = U < kHot ? U : kHot;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t rings = sbase + (uint32_t)us * 2048u;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + (size_t)us * 2048 + W * kHornerRing);
+  const uint32_t rings = sbase + (uint32_t)us * kRow;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + (size_t)us * kRow + W * kHornerRing);
   int* dyn = reinterpret_cast<int*>(tslot) + 1;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
@@ -406,9 +483,9 @@ k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tbase = *tslot;
   if (tbase != 0) __trap();  // the program's TMEM addresses assume the whole TMEM at column 0
-  SeedsH<HYB> sd;
+  SeedsH<T, HYB> sd;
   sd.tq = tbase + ((uint32_t)((warp & 3) * 32) << 16);
-  sd.sb = sbase + (uint32_t)(lane * 16);
+  sd.sb = sbase + (uint32_t)(lane * sizeof(V));
   sd.gb = nullptr;
   const uint32_t ring = rings + (uint32_t)warp * kHornerRing;
   const int32_t nops = __ldg(chunk + nchunk);  // records per quadrant copy
@@ -422,45 +499,44 @@ k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __
     const int slice = whole ? 0 : (int)((it - full_tiles) % tail_parts);
     const int nsl = whole ? 1 : tail_parts;
     const int cb = (int)((int64_t)slice * nchunk / nsl), ce = (int)((int64_t)(slice + 1) * nchunk / nsl);
-    const double2* Tt = T + tile * (int64_t)rows * 128;
+    const V* Tt = Tab + tile * (int64_t)rows * 128;
     // the next item's on-chip rows into L2 while this tile computes
     if (threadIdx.x == 0 && it + gridDim.x < nitems) {
       const int64_t nit = it + gridDim.x;
       const int64_t nt = nit < full_tiles ? nit : full_tiles + (nit - full_tiles) / tail_parts;
       if (nt != tile) {
-        const char* src = reinterpret_cast<const char*>(T + nt * (int64_t)rows * 128);
-        const uint32_t bytes = (uint32_t)(hot + us) * 2048u;
+        const char* src = reinterpret_cast<const char*>(Tab + nt * (int64_t)rows * 128);
+        const uint32_t bytes = (uint32_t)(hot + us) * kRow;
         for (uint32_t o = 0; o < bytes; o += 32768u) {
           const uint32_t n = bytes - o < 32768u ? bytes - o : 32768u;
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src + o), "r"(n) : "memory");
         }
       }
     }
-    if (HYB) sd.gb = reinterpret_cast<const char*>(Tt + (size_t)(hot + us) * 128) + lane * 16;
-    // TMEM rows: each lane quadrant's four warps write all hot rows
+    if (HYB) sd.gb = reinterpret_cast<const char*>(Tt + (size_t)(hot + us) * 128) + lane * sizeof(V);
+    // TMEM rows: each lane quadrant's W/4 warps write all hot rows
     for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (W / 4)) {
-      double2 v[4][4];
+      V v[4][4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int h = h0 + q * (W / 4);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          v[q][k] = h < hot ? ld_stream(Tt + (size_t)h * 128 + k * 32 + lane) : make_double2(0.0, 0.0);
+        for (int k = 0; k < 4; ++k) v[q][k] = h < hot ? ld_stream(Tt + (size_t)h * 128 + k * 32 + lane) : mk2(T(0), T(0));
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int h = h0 + q * (W / 4);
-        if (h < hot) {
-          tmem_st8(sd.tq + (uint32_t)h * 16, v[q][0], v[q][1]);
-          tmem_st8(sd.tq + (uint32_t)h * 16 + 8, v[q][2], v[q][3]);
-        }
+        if (h < hot) tmem_st_row(sd.tq + (uint32_t)(h * kC), v[q]);
       }
     }
     // shared rows: asynchronous 16-byte copies
-    for (int idx = threadIdx.x; idx < us * 128; idx += W * 32)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + idx * 16),
-                   "l"(Tt + (size_t)hot * 128 + idx)
-                   : "memory");
+    {
+      const char* src = reinterpret_cast<const char*>(Tt + (size_t)hot * 128);
+      const int n16 = us * (int)(kRow / 16);
+      for (int idx = threadIdx.x; idx < n16; idx += W * 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + idx * 16), "l"(src + (size_t)idx * 16)
+                     : "memory");
+    }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     if (threadIdx.x == 0) *dyn = cb + W;
@@ -474,7 +550,7 @@ k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __
       const int32_t nr = __ldg(croots + ci);
       st.begin(reinterpret_cast<const int4*>(ops) + (size_t)(warp & 3) * nops + b, (uint32_t)(e - b), ring, lane);
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int32_t k = 0; k < nr; ++k) root<NU, HYB>(st, acc, sd, lane);
+      for (int32_t k = 0; k < nr; ++k) root<NU>(st, acc, sd, lane);
 #pragma unroll
       for (int k = 0; k < 4; ++k) dst[(size_t)ci * 128 + k * 32 + lane] = acc[k];
       int nx = 0;
@@ -501,24 +577,32 @@ k2_horner(const double2* __restrict__ T, int64_t S, int U, int us, const OpH* __
 }  // namespace hdev
 
 // ------------------------------------------------------------------- host
-// warps per CTA (ACEDAG_HWARPS = 16 | 20 | 24)
-int horner_warps() {
-  static int w = [] {
+// warps per CTA: fp64 16 (ACEDAG_HWARPS = 16 | 20 | 24), fp32 32 (64
+// registers; ACEDAG_HWARPS32 = 16 | 20 | 24 | 32; 1.39 vs 1.58 ms at 16, cfg2)
+int horner_warps(bool f32) {
+  static int w64 = [] {
     const char* e = getenv("ACEDAG_HWARPS");
     const int v = e ? atoi(e) : kHornerWarps;
     return v == 20 || v == 24 ? v : 16;
   }();
-  return w;
+  static int w32 = [] {
+    const char* e = getenv("ACEDAG_HWARPS32");
+    const int v = e ? atoi(e) : 32;
+    return v == 16 || v == 20 || v == 24 ? v : 32;
+  }();
+  return f32 ? w32 : w64;
 }
 
-int horner_us_max(size_t smem_optin) {
-  const size_t fixed = (size_t)horner_warps() * kHornerRing + 16;
-  return smem_optin > fixed ? (int)((smem_optin - fixed) / 2048) : 0;
+int horner_us_max(size_t smem_optin, bool f32) {
+  const size_t fixed = (size_t)horner_warps(f32) * kHornerRing + 16;
+  return smem_optin > fixed ? (int)((smem_optin - fixed) / horner_row_bytes(f32)) : 0;
 }
-size_t horner_smem(int us) { return (size_t)us * 2048 + (size_t)horner_warps() * kHornerRing + 16; }
+size_t horner_smem(int us, bool f32) {
+  return (size_t)us * horner_row_bytes(f32) + (size_t)horner_warps(f32) * kHornerRing + 16;
+}
 
 namespace {
-uint32_t w_count(uint32_t w) { return w & 0xFFFFu; }
+uint32_t w_count(uint32_t w) { return w & 0x7FFFu; }
 // relative size of the second half of the chunks (ACEDAG_HGUIDE; 1 = equal)
 double guided_tail() {
   static double v = [] {
@@ -533,13 +617,14 @@ struct HornerEnc {
   uint32_t hot, us, U;
   int nu;
   std::vector<OpH>& out;
+  uint32_t hot_cols, row_bytes;  // TMEM columns per hot row, bytes per shared/global row
   std::vector<uint8_t> hot_rec;  // record's z is a TMEM column (gets the lane-quadrant bits per copy)
   bool ok = true;
 
   uint32_t cls(uint32_t s) const { return s < hot ? 0u : (s < hot + us ? 1u : 2u); }
   uint32_t zof(uint32_t s) const {
     const uint32_t c = cls(s);
-    return c == 0 ? s * 16u : (c == 1 ? (s - hot) * 2048u : (s - hot - us) * 2048u);
+    return c == 0 ? s * hot_cols : (c == 1 ? (s - hot) * row_bytes : (s - hot - us) * row_bytes);
   }
   static uint32_t slot(const Op& o) { return o.off / kRowBytes; }
   size_t skip(size_t pos) const {
@@ -553,8 +638,8 @@ struct HornerEnc {
     if (c == 1) ns += k;
   }
   uint32_t pack(uint32_t n, uint32_t nh, uint32_t ns) {
-    if (n > 0xFFFFu || nh > 63u || ns > 1023u) ok = false;
-    return n | nh << 16 | ns << 22;
+    if (n > 0x7FFFu || nh > 127u || ns > 1023u) ok = false;
+    return n | nh << 15 | ns << 22;
   }
   // leaves [first, first + n) of a node (positions of records with nch = 0)
   void emit_leaves(const std::vector<size_t>& kids, size_t b, size_t e) {
@@ -653,11 +738,12 @@ struct HornerEnc {
 };
 }  // namespace
 
-bool encode_horner(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<OpH>& out,
+bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::vector<OpH>& out,
                    std::vector<int32_t>& chunk, std::vector<int32_t>& croots) {
   out.clear();
   const size_t nchunk = H.chunk.size() > 0 ? H.chunk.size() - 1 : 0;
-  HornerEnc E{H, hot, us, (uint32_t)H.slot_label.size(), H.max_order, out};
+  HornerEnc E{H, hot, us, (uint32_t)H.slot_label.size(), H.max_order, out, f32 ? 8u : 16u,
+              (uint32_t)horner_row_bytes(f32)};
   // every root unit (a split root is several), with its record offset and cost
   std::vector<size_t> start;
   std::vector<double> cost;
@@ -708,6 +794,14 @@ bool encode_horner(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<OpH
   // quadrant's lane bits, so a hot fetch is R2UR + tcgen05.ld with no add
   const size_t n = out.size();
   if (E.hot_rec.size() != n) return false;
+  if (f32)  // fp32 programs carry each coefficient as a float in the low word
+    for (OpH& o : out) {
+      const float f = (float)o.c;
+      uint32_t b;
+      std::memcpy(&b, &f, 4);
+      const uint64_t u = b;
+      std::memcpy(&o.c, &u, 8);
+    }
   out.resize(4 * n);
   for (size_t q = 1; q < 4; ++q)
     for (size_t i = 0; i < n; ++i) {
@@ -717,34 +811,48 @@ bool encode_horner(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<OpH
   return E.ok && 4 * n < (size_t)INT32_MAX;
 }
 
-template <int NU, bool HYB>
-static cudaError_t launch_nu(const double2* T, int64_t S, int U, int us, const OpH* ops, const int32_t* chunk,
+template <int NU, typename T, bool HYB>
+static cudaError_t launch_nu(const void* Tab, int64_t S, int U, int us, const OpH* ops, const int32_t* chunk,
                              const int32_t* croots, int nchunk, double* out, double* part, int64_t full, int parts,
                              double* tail, int grid, cudaStream_t st) {
-  const int W = horner_warps();
-  auto k = W == 24 ? hdev::k2_horner<NU, HYB, 24> : (W == 20 ? hdev::k2_horner<NU, HYB, 20> : hdev::k2_horner<NU, HYB, 16>);
-  const size_t smem = horner_smem(us);
+  const int W = horner_warps(sizeof(T) == 4);
+  auto k = W == 24 ? hdev::k2_horner<NU, T, HYB, 24>
+                   : (W == 20 ? hdev::k2_horner<NU, T, HYB, 20> : hdev::k2_horner<NU, T, HYB, 16>);
+  if constexpr (sizeof(T) == 4) {
+    if (W == 32) k = hdev::k2_horner<NU, T, HYB, 32>;
+  }
+  const size_t smem = horner_smem(us, sizeof(T) == 4);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, W * 32, smem, st>>>(T, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail);
+  k<<<grid, W * 32, smem, st>>>(reinterpret_cast<const typename hdev::HTr<T>::V*>(Tab), S, U, us, ops, chunk, croots,
+                                nchunk, out, part, full, parts, tail);
   return cudaGetLastError();
 }
 
-cudaError_t launch_horner(int nu, const double2* T, int64_t S, int U, int us, const OpH* ops,
+cudaError_t launch_horner(int nu, bool f32, const void* Tab, int64_t S, int U, int us, const OpH* ops,
                           const int32_t* chunk, const int32_t* croots, int nchunk, double* out, double* part,
                           int64_t full, int parts, double* tail, int grid, cudaStream_t st) {
-  const int hot = std::min(U, (int)kHornerHot);
+  const int hot = std::min(U, horner_hot_rows(f32));
   const bool hyb = hot + us < U;
-#define ACEDAG_H(N)                                                                                          \
-  return hyb ? launch_nu<N, true>(T, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail, grid, \
-                                  st)                                                                        \
-             : launch_nu<N, false>(T, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail, grid, st)
+#define ACEDAG_H(N, T)                                                                                          \
+  return hyb ? launch_nu<N, T, true>(Tab, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail,  \
+                                     grid, st)                                                                \
+             : launch_nu<N, T, false>(Tab, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail, \
+                                      grid, st)
+  if (f32) {
+    switch (nu) {
+      case 2: ACEDAG_H(2, float);
+      case 3: ACEDAG_H(3, float);
+      case 4: ACEDAG_H(4, float);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (nu) {
-    case 2: ACEDAG_H(2);
-    case 3: ACEDAG_H(3);
-    case 4: ACEDAG_H(4);
-    case 5: ACEDAG_H(5);
-    case 6: ACEDAG_H(6);
+    case 2: ACEDAG_H(2, double);
+    case 3: ACEDAG_H(3, double);
+    case 4: ACEDAG_H(4, double);
+    case 5: ACEDAG_H(5, double);
+    case 6: ACEDAG_H(6, double);
     default: return cudaErrorInvalidValue;
   }
 #undef ACEDAG_H

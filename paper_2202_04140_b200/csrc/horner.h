@@ -20,10 +20,11 @@
 
 namespace acedag {
 
-// 16-byte record, read warp-uniformly.  z: the seed's class-scaled offset
-// (TMEM row -> column row*16; shared row -> byte row*2048; global row -> byte
-// row*2048).  w: nch | nhot << 16 | nsm << 22 (children by class, in that
-// order).  A root is two records; the second carries w = cls_a | cls_b << 2 |
+// 16-byte record, read warp-uniformly.  c: the coefficient (fp32 programs:
+// a float in the low word).  z: the seed's class-scaled offset (TMEM row ->
+// column row*16 (c128) or row*8 (c64) plus the lane-quadrant bits; shared /
+// global row -> byte row*2048 (c128) or row*1024 (c64)).  w: nch | nhot << 15
+// | nsm << 22 (children by class, in that order).  A root is two records; the second carries w = cls_a | cls_b << 2 |
 // single << 4 (single: an order-1 coefficient, phi += c Re(s_a)).
 struct alignas(16) OpH {
   double c;
@@ -31,7 +32,9 @@ struct alignas(16) OpH {
   uint32_t w;
 };
 
-constexpr uint32_t kHornerHot = 32;      // TMEM rows (4 sites x c128 = 16 columns each)
+constexpr uint32_t kHornerHot = 32;      // TMEM rows (4 sites x c128 = 16 columns each; c64: 64 rows)
+inline int horner_hot_rows(bool f32) { return f32 ? 64 : (int)kHornerHot; }
+inline int horner_row_bytes(bool f32) { return f32 ? 1024 : 2048; }
 constexpr int kHornerWarps = 16;
 constexpr uint32_t kHornerRing = 2048;   // per-warp program ring: 3 blocks + mirror
 // leaves per record group: a node of the last inner order with more is split
@@ -45,16 +48,16 @@ constexpr uint32_t kMaxLeaves = 30;
 // out holds four copies of the program (one per TMEM lane quadrant: hot
 // records' z carries the quadrant's lane bits), chunk offsets index copy 0.
 // Returns false when a count does not fit its field (another kernel is used).
-bool encode_horner(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<OpH>& out,
+bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::vector<OpH>& out,
                    std::vector<int32_t>& chunk, std::vector<int32_t>& croots);
 
 // shared-memory rows k2_horner can hold besides its rings
-int horner_us_max(size_t smem_optin);
-size_t horner_smem(int us);
+int horner_us_max(size_t smem_optin, bool f32);
+size_t horner_smem(int us, bool f32);
 
-// tiles: tile-major seed table [ntiles][U+1][128] c128 (k_tile_seeds<128>).
+// tiles: tile-major seed table [ntiles][U+1][128] c128 / c64 (k_tile_seeds<128>).
 // part: [grid][nchunk][128]; tail: [(ntiles - full)][nchunk][128].
-cudaError_t launch_horner(int nu, const double2* tiles, int64_t S, int U, int us, const OpH* ops,
+cudaError_t launch_horner(int nu, bool f32, const void* tiles, int64_t S, int U, int us, const OpH* ops,
                           const int32_t* chunk, const int32_t* croots, int nchunk, double* out, double* part,
                           int64_t full, int parts, double* tail, int grid, cudaStream_t st);
 

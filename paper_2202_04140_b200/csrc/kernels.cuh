@@ -1331,25 +1331,26 @@ k2_tmem4(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
 // columns in ascending order (coalesced reads of each site row); a padded
 // [32][TS + 1] shared block transposes 32 columns at a time.
 // cols: column of the j-th used entry (NULL: j); slots: its row (NULL: j).
-template <int TS>
-__global__ void __launch_bounds__(512) k_tile_seeds(const double2* __restrict__ A, int64_t S, int L,
+template <int TS, typename V = double2>
+__global__ void __launch_bounds__(512) k_tile_seeds(const V* __restrict__ A, int64_t S, int L,
                                                     const int32_t* __restrict__ cols,
                                                     const uint16_t* __restrict__ slots, int U,
-                                                    double2* __restrict__ T) {
-  extern __shared__ double2 tb[];  // [32][TS + 1]
+                                                    V* __restrict__ T) {
+  extern __shared__ __align__(16) unsigned char tbraw[];
+  V* tb = reinterpret_cast<V*>(tbraw);  // [32][TS + 1]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = 16;
   const int64_t tile = blockIdx.x;
   const int R = U + 1;
-  double2* Tt = T + tile * (int64_t)R * TS;
+  V* Tt = T + tile * (int64_t)R * TS;
   for (int j0 = 0; j0 < U; j0 += 32) {
     const int j = j0 + lane;
     const int col = j < U ? (cols ? __ldg(cols + j) : j) : -1;
-    double2 v[TS / NW];
+    V v[TS / NW];
 #pragma unroll
     for (int q = 0; q < TS / NW; ++q) {
       const int64_t site = tile * TS + warp + q * NW;
-      v[q] = (col >= 0 && site < S) ? ld_stream(A + site * L + col) : make_double2(0.0, 0.0);
+      v[q] = (col >= 0 && site < S) ? ld_stream(A + site * L + col) : V{0, 0};
     }
 #pragma unroll
     for (int q = 0; q < TS / NW; ++q) tb[lane * (TS + 1) + warp + q * NW] = v[q];
@@ -1361,7 +1362,7 @@ __global__ void __launch_bounds__(512) k_tile_seeds(const double2* __restrict__ 
     }
     __syncthreads();
   }
-  for (int q = threadIdx.x; q < TS; q += blockDim.x) Tt[(int64_t)U * TS + q] = make_double2(1.0, 0.0);
+  for (int q = threadIdx.x; q < TS; q += blockDim.x) Tt[(int64_t)U * TS + q] = V{1, 0};
 }
 
 // ------------------------------------- K2 (four sites per lane, TMEM + smem)

@@ -45,7 +45,7 @@ def compile_program(graph, node_ids, values, warps: int = 32) -> dict:
 
 
 # k2_horner records (csrc/horner.h): {coefficient, z = class-scaled seed
-# offset, w = nch | nhot << 16 | nsm << 22 (a root's second record: class
+# offset, w = nch | nhot << 15 | nsm << 22 (a root's second record: class
 # flags cls_a | cls_b << 2 | single << 4)}
 OPH_DTYPE = np.dtype([("c", "<f8"), ("z", "<u4"), ("w", "<u4")])
 HORNER_HOT, HORNER_MAX_LEAVES = 32, 30

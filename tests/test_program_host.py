@@ -108,14 +108,14 @@ def simulate_horner(h, A):
         return seeds[:, s]
 
     def cls_of(j, w):
-        nh, ns = (w >> 16) & 63, w >> 22
+        nh, ns = (w >> 15) & 127, w >> 22
         return 0 if j < nh else (1 if j < nh + ns else 2)
 
     pos = 0
 
     def leaves(w, H):
         nonlocal pos
-        n = w & 0xFFFF
+        n = w & 0x7FFF
         assert n <= HORNER_MAX_LEAVES
         for j in range(n):
             r = ops[pos]
@@ -126,7 +126,7 @@ def simulate_horner(h, A):
 
     def children(w, D, Hp):
         nonlocal pos
-        for j in range(w & 0xFFFF):
+        for j in range(w & 0x7FFF):
             r = ops[pos]
             pos += 1
             H = np.full(A.shape[0], r["c"], complex)

@@ -581,9 +581,10 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   for (int f = 0; f < 2; ++f) {
     acedag_plan::HornerProg& hp = P->hp[f];
     hp.ok = false;
-    if ((k2_mode() == 5 && H.max_order <= 4) || (k2_mode() == 9 && (f == 0 || H.max_order <= 4))) {
+    // fp64: order <= 4 (order 5-6 spill; on request only); fp32: order <= 6
+    if ((k2_mode() == 5 && H.max_order <= (f == 1 ? 6 : 4)) || k2_mode() == 9) {
       const int hot = std::min(P->U, horner_hot_rows(f == 1));
-      hp.us = std::min(P->U - hot, horner_us_max(P->smem_optin, f == 1));
+      hp.us = std::min(P->U - hot, horner_us_max(P->smem_optin, f == 1, H.max_order));
       std::vector<OpH> oh;
       std::vector<int32_t> ch, cr;
       hp.ok = encode_horner(H, f == 1, (uint32_t)hot, (uint32_t)hp.us, oh, ch, cr);
@@ -1095,7 +1096,7 @@ bool run_horner(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
 bool use_horner(const acedag_plan* P, int64_t S, bool f32 = false) {
   (void)S;
   const acedag_plan::HornerProg& hp = P->hp[f32 ? 1 : 0];
-  return hp.ok && ((P->host.max_order <= 4 && k2_mode() == 5) || k2_mode() == 9);
+  return hp.ok && ((P->host.max_order <= (f32 ? 6 : 4) && k2_mode() == 5) || k2_mode() == 9);
 }
 
 template <int NU> struct QuadF64 {

@@ -577,9 +577,10 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
 }  // namespace hdev
 
 // ------------------------------------------------------------------- host
-// warps per CTA: fp64 16 (ACEDAG_HWARPS = 16 | 20 | 24), fp32 32 (64
-// registers; ACEDAG_HWARPS32 = 16 | 20 | 24 | 32; 1.39 vs 1.58 ms at 16, cfg2)
-int horner_warps(bool f32) {
+// warps per CTA: fp64 16 (ACEDAG_HWARPS = 16 | 20 | 24); fp32 32 for
+// order <= 4 (64 registers; 1.39 vs 1.58 ms at 16, cfg2), 16 above (one
+// more accumulator per level; ACEDAG_HWARPS32 = 16 | 20 | 24 | 32 overrides)
+int horner_warps(bool f32, int nu) {
   static int w64 = [] {
     const char* e = getenv("ACEDAG_HWARPS");
     const int v = e ? atoi(e) : kHornerWarps;
@@ -587,18 +588,20 @@ int horner_warps(bool f32) {
   }();
   static int w32 = [] {
     const char* e = getenv("ACEDAG_HWARPS32");
-    const int v = e ? atoi(e) : 32;
-    return v == 16 || v == 20 || v == 24 ? v : 32;
+    const int v = e ? atoi(e) : 0;
+    return v == 16 || v == 20 || v == 24 || v == 32 ? v : 0;
   }();
-  return f32 ? w32 : w64;
+  if (!f32) return w64;
+  if (w32) return w32;
+  return nu <= 4 ? 32 : 16;
 }
 
-int horner_us_max(size_t smem_optin, bool f32) {
-  const size_t fixed = (size_t)horner_warps(f32) * kHornerRing + 16;
+int horner_us_max(size_t smem_optin, bool f32, int nu) {
+  const size_t fixed = (size_t)horner_warps(f32, nu) * kHornerRing + 16;
   return smem_optin > fixed ? (int)((smem_optin - fixed) / horner_row_bytes(f32)) : 0;
 }
-size_t horner_smem(int us, bool f32) {
-  return (size_t)us * horner_row_bytes(f32) + (size_t)horner_warps(f32) * kHornerRing + 16;
+size_t horner_smem(int us, bool f32, int nu) {
+  return (size_t)us * horner_row_bytes(f32) + (size_t)horner_warps(f32, nu) * kHornerRing + 16;
 }
 
 namespace {
@@ -815,13 +818,13 @@ template <int NU, typename T, bool HYB>
 static cudaError_t launch_nu(const void* Tab, int64_t S, int U, int us, const OpH* ops, const int32_t* chunk,
                              const int32_t* croots, int nchunk, double* out, double* part, int64_t full, int parts,
                              double* tail, int grid, cudaStream_t st) {
-  const int W = horner_warps(sizeof(T) == 4);
+  const int W = horner_warps(sizeof(T) == 4, NU);
   auto k = W == 24 ? hdev::k2_horner<NU, T, HYB, 24>
                    : (W == 20 ? hdev::k2_horner<NU, T, HYB, 20> : hdev::k2_horner<NU, T, HYB, 16>);
   if constexpr (sizeof(T) == 4) {
     if (W == 32) k = hdev::k2_horner<NU, T, HYB, 32>;
   }
-  const size_t smem = horner_smem(us, sizeof(T) == 4);
+  const size_t smem = horner_smem(us, sizeof(T) == 4, NU);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, W * 32, smem, st>>>(reinterpret_cast<const typename hdev::HTr<T>::V*>(Tab), S, U, us, ops, chunk, croots,
@@ -844,6 +847,8 @@ cudaError_t launch_horner(int nu, bool f32, const void* Tab, int64_t S, int U, i
       case 2: ACEDAG_H(2, float);
       case 3: ACEDAG_H(3, float);
       case 4: ACEDAG_H(4, float);
+      case 5: ACEDAG_H(5, float);
+      case 6: ACEDAG_H(6, float);
       default: return cudaErrorInvalidValue;
     }
   }

@@ -52,8 +52,8 @@ bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::
                    std::vector<int32_t>& chunk, std::vector<int32_t>& croots);
 
 // shared-memory rows k2_horner can hold besides its rings
-int horner_us_max(size_t smem_optin, bool f32);
-size_t horner_smem(int us, bool f32);
+int horner_us_max(size_t smem_optin, bool f32, int nu);
+size_t horner_smem(int us, bool f32, int nu);
 
 // tiles: tile-major seed table [ntiles][U+1][128] c128 / c64 (k_tile_seeds<128>).
 // part: [grid][nchunk][128]; tail: [(ntiles - full)][nchunk][128].

@@ -1720,9 +1720,35 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
     int rc2 = full_triples(dev, cap, &tri, &ntri);
     if (rc2) return rc2;
   }
-  CK(cudaFuncSetAttribute(dev::pool_positions2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dev::pool_positions2<<<grid, 256, smem, st>>>(xyz, counts, S, J, cap, r_in, r_cut, tri, ntri, col_of,
-                                                stride, out); note_launch();
+  // v4 (compile-time degree cap, warp per site) for caps 12 and 14 when the
+  // triples fit its accumulators; ACEDAG_POOL=2 forces v2 (CTA per site)
+  static const bool force_v2 = getenv("ACEDAG_POOL") && atoi(getenv("ACEDAG_POOL")) == 2;
+  bool done = false;
+  if (!force_v2 && (cap == 12 || cap == 14) && ntri <= 32 * 16) {
+    auto launch4 = [&](auto k, int W, size_t wb) -> cudaError_t {
+      const size_t sm4 = (size_t)W * wb;
+      cudaError_t e4 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
+      if (e4 != cudaSuccess) return e4;
+      const int g4 = (int)std::min<int64_t>((S + W - 1) / W, (int64_t)sms * 64);
+      k<<<g4, W * 32, sm4, st>>>(xyz, counts, S, J, r_in, r_cut, tri, ntri, col_of, stride, out);
+      return cudaGetLastError();
+    };
+    cudaError_t e4;
+    if (cap == 12)
+      e4 = ntri <= 256 ? launch4(dev::pool_positions4<12, 8>, dev::Pool4Geom<12>::kW, dev::Pool4Geom<12>::kWarpBytes)
+                       : launch4(dev::pool_positions4<12, 16>, dev::Pool4Geom<12>::kW, dev::Pool4Geom<12>::kWarpBytes);
+    else
+      e4 = ntri <= 256 ? launch4(dev::pool_positions4<14, 8>, dev::Pool4Geom<14>::kW, dev::Pool4Geom<14>::kWarpBytes)
+                       : launch4(dev::pool_positions4<14, 16>, dev::Pool4Geom<14>::kW, dev::Pool4Geom<14>::kWarpBytes);
+    note_launch();
+    if (e4 != cudaSuccess) return cuda_fail(e4, "pool_positions4");
+    done = true;
+  }
+  if (!done) {
+    CK(cudaFuncSetAttribute(dev::pool_positions2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dev::pool_positions2<<<grid, 256, smem, st>>>(xyz, counts, S, J, cap, r_in, r_cut, tri, ntri, col_of,
+                                                  stride, out); note_launch();
+  }
   (void)labels;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "pool_positions");

@@ -312,3 +312,146 @@ inline size_t pool2_smem(int cap, int J) {
 
 }  // namespace dev
 }  // namespace acedag
+
+namespace acedag {
+namespace dev {
+
+// ------------------------------------------------------- positions, v4
+// Degree cap as a template parameter (cfg2/3: 12, cfg5: 14): one WARP per
+// site, lane = neighbour.  Each lane evaluates its neighbour's weighted
+// radial row and the whole Y_lm table (m outer, the upward Legendre
+// recursion in l inner) as straight-line code with compile-time indices
+// and constants -- no per-(j, m) work items, no divergent trip counts --
+// into shared memory Y[j][pair] (row stride odd in 16-B units: conflict-free
+// for both the lane = j writes and the lane = triple reads).  Then every
+// lane accumulates its TPL (n, l, m >= 0) triples A = sum_j WR[j][n] Y[j][lm]
+// in registers, j ascending, NB neighbours per pass.
+template <int CAP, int NB = 16>
+struct Pool4Geom {
+  static constexpr int kNB = NB;  // neighbours per pass (lanes computing Y)
+  static constexpr int kC1 = CAP + 1;
+  static constexpr int kNP = kC1 * (CAP + 2) / 2;
+  static constexpr int kNPp = kNP | 1;  // odd stride (16-B units)
+  static constexpr size_t kWarpBytes = (size_t)NB * kNPp * 16 + (size_t)NB * kC1 * 8;
+  static constexpr int kW = (int)((227 * 1024) / kWarpBytes) < 16 ? (int)((227 * 1024) / kWarpBytes) : 16;
+};
+
+template <int CAP, int TPL>
+__global__ void __launch_bounds__(Pool4Geom<CAP>::kW * 32)
+pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ counts, int64_t S, int J, double r_in,
+                double r_cut, const int4* __restrict__ tri, int ntri, const int32_t* __restrict__ col_of,
+                int64_t out_stride, double2* __restrict__ out) {
+  using G = Pool4Geom<CAP>;
+  constexpr int C1 = G::kC1, NPp = G::kNPp, W = G::kW, NB = G::kNB;
+  extern __shared__ __align__(16) unsigned char psm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* Y = reinterpret_cast<double2*>(psm + G::kWarpBytes * warp);  // [NB][NPp]
+  double* WR = reinterpret_cast<double*>(Y + NB * NPp);                 // [NB][C1]
+  const double inv_span = 1.0 / (r_cut - r_in);
+  int tq[TPL];  // this lane's triples: pair << 8 | n (-1: none)
+#pragma unroll
+  for (int t = 0; t < TPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < ntri) {
+      const int4 q = __ldg(tri + i);
+      tq[t] = (q.y * (q.y + 1) / 2 + q.z) << 8 | q.x;
+    } else {
+      tq[t] = -1;
+    }
+  }
+  for (int64_t s = (int64_t)blockIdx.x * W + warp; s < S; s += (int64_t)gridDim.x * W) {
+    const int nj = counts ? min(counts[s], J) : J;
+    double2 acc[TPL];
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) acc[t] = make_double2(0.0, 0.0);
+    for (int j0 = 0; j0 < nj; j0 += NB) {
+      const int nb = min(NB, nj - j0);
+      if (lane < nb) {
+        const double* p = xyz + (s * J + j0 + lane) * 3;
+        const double x = p[0], y = p[1], z = p[2];
+        const double rho2 = x * x + y * y;
+        const double r = sqrt(rho2 + z * z);
+        const double w = r < r_cut ? 0.5 * (1.0 + cospi(r / r_cut)) : 0.0;
+        const double u = 2.0 * fmin(1.0, fmax(0.0, (r - r_in) * inv_span)) - 1.0;
+        double* wr = WR + lane * C1;
+        {
+          double t0 = 1.0, t1 = u;
+          wr[0] = w;
+          if (CAP >= 1) wr[1] = w * u;
+#pragma unroll
+          for (int n = 2; n <= CAP; ++n) {
+            const double t2 = 2.0 * u * t1 - t0;
+            wr[n] = w * t2;
+            t0 = t1;
+            t1 = t2;
+          }
+        }
+        const double rho = sqrt(rho2);
+        const double ct = r > 0.0 ? z / r : 1.0, st = r > 0.0 ? rho / r : 0.0;
+        const double cp = rho > 0.0 ? x / rho : 1.0, sp = rho > 0.0 ? y / rho : 0.0;
+        double2* yj = Y + lane * NPp;
+        double ec = 1.0, es = 0.0, pmm = 1.0;
+#pragma unroll
+        for (int m = 0; m <= CAP; ++m) {
+          if (m > 0) {
+            const double nc = ec * cp - es * sp;
+            es = ec * sp + es * cp;
+            ec = nc;
+            pmm *= -(2.0 * m - 1.0) * st;
+          }
+          double nv = c_ylm_norm[m * (m + 1) / 2 + m] * pmm;
+          yj[m * (m + 1) / 2 + m] = make_double2(nv * ec, nv * es);
+          if (m + 1 <= CAP) {
+            double p0 = pmm, p1 = ct * (2.0 * m + 1.0) * pmm;
+            nv = c_ylm_norm[(m + 1) * (m + 2) / 2 + m] * p1;
+            yj[(m + 1) * (m + 2) / 2 + m] = make_double2(nv * ec, nv * es);
+#pragma unroll
+            for (int l = m + 2; l <= CAP; ++l) {
+              const double p2 = (ct * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) * c_recip[l - m];
+              nv = c_ylm_norm[l * (l + 1) / 2 + m] * p2;
+              yj[l * (l + 1) / 2 + m] = make_double2(nv * ec, nv * es);
+              p0 = p1;
+              p1 = p2;
+            }
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < TPL; ++t) {
+        if (tq[t] >= 0) {
+          const int n = tq[t] & 255, pair = tq[t] >> 8;
+          const double2* yp = Y + pair;
+          const double* wp = WR + n;
+          double ax = acc[t].x, ay = acc[t].y;
+#pragma unroll 4
+          for (int jj = 0; jj < nb; ++jj) {
+            const double2 yv = yp[jj * NPp];
+            const double a = wp[jj * C1];
+            ax += a * yv.x;
+            ay += a * yv.y;
+          }
+          acc[t] = make_double2(ax, ay);
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int t = 0; t < TPL; ++t) {
+      if (tq[t] >= 0) {
+        const int4 q = __ldg(tri + lane + 32 * t);
+        const int cpos = col_of ? col_of[q.w] : q.w;
+        if (cpos >= 0) out[s * out_stride + cpos] = acc[t];
+        if (q.z > 0) {  // A[n, l, -m] = (-1)^m conj(A[n, l, m])
+          const int lab_m = q.w - 2 * q.z;
+          const int cm = col_of ? col_of[lab_m] : lab_m;
+          const double sg = (q.z & 1) ? -1.0 : 1.0;
+          if (cm >= 0) out[s * out_stride + cm] = make_double2(sg * acc[t].x, -sg * acc[t].y);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace acedag

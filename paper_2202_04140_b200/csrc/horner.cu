@@ -577,21 +577,17 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
 }  // namespace hdev
 
 // ------------------------------------------------------------------- host
-// warps per CTA: fp64 16 (ACEDAG_HWARPS = 16 | 20 | 24); fp32 32 for
-// order <= 4 (64 registers; 1.39 vs 1.58 ms at 16, cfg2), 16 above (one
-// more accumulator per level; ACEDAG_HWARPS32 = 16 | 20 | 24 | 32 overrides)
+// warps per CTA: fp64 16 (128 registers; 20 and 24 warps spill and ran
+// 7% / 17% slower at cfg2); fp32 32 for order <= 4 (64 registers; 1.39 vs
+// 1.58 ms at 16, cfg2), 16 above (one more accumulator per level; 20 ran
+// 611 vs 528 ms at cfg4).  ACEDAG_HWARPS32 = 16 | 32 overrides for fp32.
 int horner_warps(bool f32, int nu) {
-  static int w64 = [] {
-    const char* e = getenv("ACEDAG_HWARPS");
-    const int v = e ? atoi(e) : kHornerWarps;
-    return v == 20 || v == 24 ? v : 16;
-  }();
   static int w32 = [] {
     const char* e = getenv("ACEDAG_HWARPS32");
     const int v = e ? atoi(e) : 0;
-    return v == 16 || v == 20 || v == 24 || v == 32 ? v : 0;
+    return v == 16 || v == 32 ? v : 0;
   }();
-  if (!f32) return w64;
+  if (!f32) return kHornerWarps;
   if (w32) return w32;
   return nu <= 4 ? 32 : 16;
 }
@@ -819,8 +815,7 @@ static cudaError_t launch_nu(const void* Tab, int64_t S, int U, int us, const Op
                              const int32_t* croots, int nchunk, double* out, double* part, int64_t full, int parts,
                              double* tail, int grid, cudaStream_t st) {
   const int W = horner_warps(sizeof(T) == 4, NU);
-  auto k = W == 24 ? hdev::k2_horner<NU, T, HYB, 24>
-                   : (W == 20 ? hdev::k2_horner<NU, T, HYB, 20> : hdev::k2_horner<NU, T, HYB, 16>);
+  auto k = hdev::k2_horner<NU, T, HYB, 16>;
   if constexpr (sizeof(T) == 4) {
     if (W == 32) k = hdev::k2_horner<NU, T, HYB, 32>;
   }

@@ -932,12 +932,9 @@ bool tile_seeds(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
   e = ws->tiles.alloc((size_t)ntiles * (P->U + 1) * TS);
   if (e != cudaSuccess) return true;
   constexpr size_t tsm = 32 * (TS + 1) * sizeof(V);
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(dev::k_tile_seeds<TS, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-    if (e != cudaSuccess) return true;
-    attr = true;
-  }
+  // per call: the attribute is per device, and plans may live on several
+  e = cudaFuncSetAttribute(dev::k_tile_seeds<TS, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+  if (e != cudaSuccess) return true;
   dev::k_tile_seeds<TS, V><<<(unsigned)ntiles, 512, tsm, st>>>(A, S, L, cols, slots, P->U,
                                                                    reinterpret_cast<V*>(ws->tiles.p)); note_launch();
   e = cudaGetLastError();

@@ -349,3 +349,52 @@ def test_all_groups_and_specs_through_k2_k3(cuda, group, p, D, nu, alg, n):
         assert ok, (method, worst)
     ok, worst = phi_gate(plan.evaluate(At.to(torch.complex64)).cpu().numpy(), pr, scale, tol=1e-5)
     assert ok, ("fp32", worst)
+
+
+def test_fp32_horner_many_tiles_and_batch_independent(cuda, cfg2):
+    """The fp32 k2_horner over more tiles than SMs (tail split): within 1e-5
+    of the oracle, and a site's value independent of its batch."""
+    S = 20_001
+    A = seeded_A(S, cfg2.num_seeds, 41).astype(np.complex64)
+    c = np.random.default_rng(42).normal(size=len(cfg2.target_ids))
+    plan = P.SitePlan(cfg2).set_coefficients(node_ids=cfg2.target_ids, values=c)
+    assert plan.kernel_name(prec="f32", sites=S) == "k2_horner (fp32)"
+    At = torch.from_numpy(A).to(cuda)
+    full = plan.evaluate(At)
+    idx = [0, 12_345, S - 1]
+    pr, _, scale = _oracle_phi(cfg2, A[idx].astype(np.complex128), cfg2.target_ids, c)
+    ok, worst = phi_gate(full.cpu().numpy()[idx], pr, scale, tol=1e-5)
+    assert ok, worst
+    assert torch.equal(plan.evaluate(At[12_000:12_700]), full[12_000:12_700])
+
+
+@pytest.mark.parametrize("cap,J", [(12, 30), (14, 40)])
+def test_pool_v4_matches_v2(cuda, cap, J):
+    """pool_positions4 (compile-time cap, warp per site) agrees with the
+    CTA-per-site pool_positions2 (ACEDAG_POOL=2, in a subprocess) to
+    1e-13 (1 + |A|), with ragged neighbour counts."""
+    import os
+    import subprocess
+    import sys
+    code = rf'''
+import numpy as np, torch, sys
+import paper_2202_04140_b200 as P
+rng = np.random.default_rng({cap})
+S = 300
+d = rng.normal(size=(S, {J}, 3)); d /= np.linalg.norm(d, axis=2, keepdims=True)
+r = (0.8 ** 3 + rng.uniform(size=(S, {J}, 1)) * (5.0 ** 3 - 0.8 ** 3)) ** (1 / 3)
+xyz = torch.from_numpy(d * r).cuda()
+counts = torch.from_numpy(rng.integers(0, {J} + 1, S).astype(np.int32)).cuda()
+np.save(sys.argv[1], P.pool_positions({cap}, xyz, counts).cpu().numpy())
+'''
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for v in ("4", "2"):
+            path = os.path.join(tmp, f"pool_v{v}.npy")
+            r = subprocess.run([sys.executable, "-c", code, path], cwd=root,
+                               env={**os.environ, "ACEDAG_POOL": v}, capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            out[v] = np.load(path)
+    assert np.all(np.abs(out["4"] - out["2"]) <= 1e-13 * (1 + np.abs(out["2"])))

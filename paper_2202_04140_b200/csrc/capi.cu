@@ -1067,7 +1067,7 @@ bool run_horner(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
   // fewer tiles than SMs: the grid covers program slices of them too
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles * 8, P->sms - t_sm_reserve));
   const int nch = nchunks(P);
-  e = lc.ws->part.alloc((size_t)grid * nch * 128);
+  e = lc.ws->part.alloc((size_t)grid * nch * 128 * 2);  // double-buffered per CTA
   if (e != cudaSuccess) return true;
   int64_t full = ntiles;
   int parts = 1;

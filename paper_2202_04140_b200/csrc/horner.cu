@@ -489,7 +489,20 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
   sd.gb = nullptr;
   const uint32_t ring = rings + (uint32_t)warp * kHornerRing;
   const int32_t nops = __ldg(chunk + nchunk);  // records per quadrant copy
-  double* mypart = part + (size_t)blockIdx.x * nchunk * 128;
+  // two partial buffers: a whole tile's chunk partials are summed by warps
+  // 0-3 at the start of the CTA's next item (hidden by the dynamic chunk
+  // hand-out) instead of in a barrier bubble at the tile end
+  double* mypart0 = part + (size_t)blockIdx.x * nchunk * 128 * 2;
+  int pbuf = 0;
+  int64_t pend_tile = -1;
+  auto sum_tile = [&](int64_t t, const double* src) {
+    const int i = threadIdx.x;  // warps 0-3: site t * 128 + i
+    double s = 0.0;
+#pragma unroll 16
+    for (int ci = 0; ci < nchunk; ++ci) s += __ldcg(src + (size_t)ci * 128 + i);
+    const int64_t site = t * 128 + i;
+    if (site < S) out[site] = s;
+  };
   RingH st;
   const int64_t ntiles = (S + 127) / 128;
   const int64_t nitems = full_tiles + (ntiles - full_tiles) * tail_parts;
@@ -544,6 +557,8 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (pend_tile >= 0 && warp < 4) sum_tile(pend_tile, mypart0 + (size_t)(pbuf ^ 1) * nchunk * 128);
+    double* mypart = mypart0 + (size_t)pbuf * nchunk * 128;
     double* dst = whole ? mypart : tailbuf + (size_t)((it - full_tiles) / tail_parts) * nchunk * 128;
     for (int ci = cb + warp; ci < ce;) {
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
@@ -561,14 +576,10 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
-    if (whole && threadIdx.x < 128) {
-      double s = 0.0;
-#pragma unroll 16
-      for (int ci = 0; ci < nchunk; ++ci) s += __ldcg(mypart + (size_t)ci * 128 + threadIdx.x);
-      const int64_t site = tile * 128 + threadIdx.x;
-      if (site < S) out[site] = s;
-    }
+    pend_tile = whole ? tile : -1;
+    if (whole) pbuf ^= 1;
   }
+  if (pend_tile >= 0 && warp < 4) sum_tile(pend_tile, mypart0 + (size_t)(pbuf ^ 1) * nchunk * 128);
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));

@@ -56,7 +56,7 @@ int horner_us_max(size_t smem_optin, bool f32, int nu);
 size_t horner_smem(int us, bool f32, int nu);
 
 // tiles: tile-major seed table [ntiles][U+1][128] c128 / c64 (k_tile_seeds<128>).
-// part: [grid][nchunk][128]; tail: [(ntiles - full)][nchunk][128].
+// part: [grid][2][nchunk][128]; tail: [(ntiles - full)][nchunk][128].
 cudaError_t launch_horner(int nu, bool f32, const void* tiles, int64_t S, int U, int us, const OpH* ops,
                           const int32_t* chunk, const int32_t* croots, int nchunk, double* out, double* part,
                           int64_t full, int parts, double* tail, int grid, cudaStream_t st);

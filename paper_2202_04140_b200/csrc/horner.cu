@@ -622,6 +622,15 @@ double guided_tail() {
   }();
   return v;
 }
+// extra chunk-cost weight of a shared-memory / global-tail seed fetch (a
+// record costs 1 (leaf) or 3 (node)); measured at cfg2: (0, 0) 2.115 ms,
+// (1, 8) 2.083, (1, 12) 2.082, (2, 20) 2.103 -- the chunks' real cost is
+// dominated by their L2 fetches.  ACEDAG_HCOST_S / ACEDAG_HCOST_G override.
+double class_cost(uint8_t cls) {
+  static double ws = [] { const char* e = getenv("ACEDAG_HCOST_S"); return e ? atof(e) : 1.0; }();
+  static double wg = [] { const char* e = getenv("ACEDAG_HCOST_G"); return e ? atof(e) : 10.0; }();
+  return cls == 1 ? ws : (cls == 2 ? wg : 0.0);
+}
 struct HornerEnc {
   const PlanHost& H;
   uint32_t hot, us, U;
@@ -629,6 +638,7 @@ struct HornerEnc {
   std::vector<OpH>& out;
   uint32_t hot_cols, row_bytes;  // TMEM columns per hot row, bytes per shared/global row
   std::vector<uint8_t> hot_rec;  // record's z is a TMEM column (gets the lane-quadrant bits per copy)
+  std::vector<uint8_t> cls_rec;  // seed class of each record (chunk cost model)
   bool ok = true;
 
   uint32_t cls(uint32_t s) const { return s < hot ? 0u : (s < hot + us ? 1u : 2u); }
@@ -657,6 +667,7 @@ struct HornerEnc {
       const Op& l = H.ops[kids[j]];
       out.push_back(OpH{l.c, zof(slot(l)), 0u});
       hot_rec.push_back(cls(slot(l)) == 0);
+      cls_rec.push_back((uint8_t)cls(slot(l)));
     }
   }
   uint32_t leaf_w(const std::vector<size_t>& kids, size_t b, size_t e) {
@@ -680,10 +691,11 @@ struct HornerEnc {
     const Op& o = H.ops[pos];
     const uint32_t z = zof(slot(o));
     const std::vector<size_t> kids = kids_of(pos);
-    const uint8_t zh = cls(slot(o)) == 0;
+    const uint8_t zh = cls(slot(o)) == 0, zc = (uint8_t)cls(slot(o));
     if (d == nu) {
       out.push_back(OpH{o.c, z, 0u});
       hot_rec.push_back(zh);
+      cls_rec.push_back(zc);
       return 1;
     }
     if (d == nu - 1) {
@@ -693,6 +705,7 @@ struct HornerEnc {
         const size_t e = std::min(kids.size(), b + kMaxLeaves);
         out.push_back(OpH{b == 0 ? o.c : 0.0, z, leaf_w(kids, b, e)});
         hot_rec.push_back(zh);
+        cls_rec.push_back(zc);
         emit_leaves(kids, b, e);
         copies++;
         b = e;
@@ -702,6 +715,7 @@ struct HornerEnc {
     const size_t me = out.size();
     out.push_back(OpH{o.c, z, 0u});
     hot_rec.push_back(zh);
+    cls_rec.push_back(zc);
     uint32_t n = 0, nh = 0, ns = 0;
     for (size_t k : kids) count(cls(slot(H.ops[k])), node(k, d + 1), n, nh, ns);
     out[me].w = pack(n, nh, ns);
@@ -724,6 +738,8 @@ struct HornerEnc {
         out.push_back(OpH{0.0, single ? 0u : zof(sb), fl});
         hot_rec.push_back(cls(sa) == 0);
         hot_rec.push_back(!single && cls(sb) == 0);
+        cls_rec.push_back((uint8_t)cls(sa));
+        cls_rec.push_back((uint8_t)(single ? 0 : cls(sb)));
         emit_leaves(kids, bb, e);
         nroots++;
         first = false;
@@ -735,6 +751,8 @@ struct HornerEnc {
       out.push_back(OpH{0.0, single ? 0u : zof(sb), fl});
       hot_rec.push_back(cls(sa) == 0);
       hot_rec.push_back(!single && cls(sb) == 0);
+      cls_rec.push_back((uint8_t)cls(sa));
+      cls_rec.push_back((uint8_t)(single ? 0 : cls(sb)));
       uint32_t n = 0, nh = 0, ns = 0;
       for (size_t k : kids) count(cls(slot(H.ops[k])), node(k, 3), n, nh, ns);
       out[me].w = pack(n, nh, ns);
@@ -769,7 +787,8 @@ bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::
         const size_t e = E.nroots - r0 == 1 ? out.size() : q + 2 + w_count(out[q].w);
         start.push_back(q);
         double c = 2.0;
-        for (size_t t = q; t < e; ++t) c += (t != q + 1 && out[t].w) ? 3.0 : 1.0;
+        for (size_t t = q; t < e; ++t)
+          c += ((t != q + 1 && out[t].w) ? 3.0 : 1.0) + class_cost(E.cls_rec[t]);
         cost.push_back(c);
         q = e;
       }

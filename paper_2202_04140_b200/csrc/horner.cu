@@ -623,12 +623,20 @@ double guided_tail() {
   return v;
 }
 // extra chunk-cost weight of a shared-memory / global-tail seed fetch (a
-// record costs 1 (leaf) or 3 (node)); measured at cfg2: (0, 0) 2.115 ms,
-// (1, 8) 2.083, (1, 12) 2.082, (2, 20) 2.103 -- the chunks' real cost is
-// dominated by their L2 fetches.  ACEDAG_HCOST_S / ACEDAG_HCOST_G override.
+// record costs 1 (leaf) or cost_w(1) (node), a root unit cost_w(2) more);
+// measured at cfg2 (node, root, shared, global): (3, 2, 0, 0) 2.115 ms,
+// (3, 2, 1, 10) 2.081, (2, 4, 0.5, 8) 2.071, (3, 8, 1, 10) 2.102 -- a chunk's
+// real time follows its L2 fetches.  ACEDAG_HCOST_S / ACEDAG_HCOST_G override.
+// record weights: [1] a node record (leaf = 1), [2] extra per root unit
+// (ACEDAG_HCOST_N / ACEDAG_HCOST_R)
+double cost_w(int which) {
+  static double wn = [] { const char* e = getenv("ACEDAG_HCOST_N"); return e ? atof(e) : 2.0; }();
+  static double wr = [] { const char* e = getenv("ACEDAG_HCOST_R"); return e ? atof(e) : 4.0; }();
+  return which == 1 ? wn : wr;
+}
 double class_cost(uint8_t cls) {
-  static double ws = [] { const char* e = getenv("ACEDAG_HCOST_S"); return e ? atof(e) : 1.0; }();
-  static double wg = [] { const char* e = getenv("ACEDAG_HCOST_G"); return e ? atof(e) : 10.0; }();
+  static double ws = [] { const char* e = getenv("ACEDAG_HCOST_S"); return e ? atof(e) : 0.5; }();
+  static double wg = [] { const char* e = getenv("ACEDAG_HCOST_G"); return e ? atof(e) : 8.0; }();
   return cls == 1 ? ws : (cls == 2 ? wg : 0.0);
 }
 struct HornerEnc {
@@ -786,9 +794,9 @@ bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::
       for (int32_t k = r0; k < E.nroots; ++k) {
         const size_t e = E.nroots - r0 == 1 ? out.size() : q + 2 + w_count(out[q].w);
         start.push_back(q);
-        double c = 2.0;
+        double c = cost_w(2);
         for (size_t t = q; t < e; ++t)
-          c += ((t != q + 1 && out[t].w) ? 3.0 : 1.0) + class_cost(E.cls_rec[t]);
+          c += ((t != q + 1 && out[t].w) ? cost_w(1) : 1.0) + class_cost(E.cls_rec[t]);
         cost.push_back(c);
         q = e;
       }

@@ -1,20 +1,25 @@
 // K2 Horner kernel: the recursive program evaluated bottom-up (see horner.h).
 //
-// Geometry (as k2_quad): one persistent CTA per SM, 16 warps, 128-site tiles;
-// lane l carries sites l, l+32, l+64, l+96 of the tile, so every program
-// record serves four products per lane.  The seeds of a tile are split by
-// use count: the 32 hottest rows in tensor memory (16 columns per lane, one
-// tcgen05.ld.32x32b.x16 per fetch, replicated in the four lane quadrants),
-// the next `us` rows in shared memory ([row][4][32] c128, conflict-free
-// LDS.128), the tail read in place from the tile-major table (L2).
+// Geometry: one persistent CTA per SM, 128-site tiles; lane l carries sites
+// l, l+32, l+64, l+96 of the tile, so every program record serves four
+// products per lane.  The seeds of a tile are split by use count: the hottest
+// rows in tensor memory (fp64: 32 rows of 16 columns per lane, one
+// tcgen05.ld.32x32b.x16 per fetch; fp32: 64 rows of 8 columns; replicated in
+// the four lane quadrants), the next `us` rows in shared memory ([row][4][32],
+// conflict-free 16-B or 8-B loads), the tail read in place from the
+// tile-major table (L2).  fp64 runs 16 warps x 128 registers, fp32 32 x 64
+// (16 above order 4).
 //
 // Per warp, the program records of a chunk stream global -> a 3-block shared
 // ring (cp.async, one 512-B block per refill) whose block 0 is mirrored past
 // block 2, so any 32 consecutive records from a checked position are
 // readable without wrap logic; the refill check runs once per "unit" (a root
 // pair, an inner record, or a deepest-level parent with its leaves), not per
-// record.  The leaf loop is then: LDS.128 record, one TMEM (or four LDS.128)
-// seed fetch, 8 DFMA.
+// record.  The leaf loop is then: LDS.128 record, one TMEM (or four LDS)
+// seed fetch, 8 FMAs.  Chunks of roots are handed to warps dynamically; each
+// chunk's per-site partial is stored and the tile's partials are summed in
+// chunk order by warps 0-3 at the start of the CTA's next item (double
+// buffer), so a site's value does not depend on the batch, grid or split.
 #include <cuda_runtime.h>
 #include <stdint.h>
 

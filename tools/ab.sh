@@ -1,5 +1,7 @@
 #!/bin/bash
-# A/B: bench each library variant twice, interleaved
+# A/B: bench each library variant twice, interleaved.  usage (on the GPU
+# box): tools/ab.sh base variant -- with abtest/base.so and abtest/variant.so
+# built here (drop abtest/ from .gpurunignore for the call).
 for rep in 1 2; do
 for v in "$@"; do
   cp abtest/$v.so paper_2202_04140_b200/libacedag_b200.so

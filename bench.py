@@ -42,16 +42,21 @@ R_IN, R_CUT = 0.8, 5.0
 
 CONFIGS = {
     "cfg1": {"D": 8, "nu": 3, "sites": 1_000, "input": "A", "n_out": 1, "scaling": "weak", "cpu_sites": 64,
+             "sha256": "ff6f09143cbc28f844d568e9ad810f830a215cab27570f8db4d757801e099b09",
              "desc": "cfg1 (BASELINE configs[0]): O3 D=8 nu<=3, 1e3 sites/GPU, A-given"},
     "cfg2": {"D": 12, "nu": 4, "sites": 100_000, "input": "A", "n_out": 1, "scaling": "weak", "cpu_sites": 32,
+             "sha256": "cf46bc8f5590ee62f6f33a4ef6e8e1d14d972d2e4db4744d64edfff5215bd6bd",
              "desc": "cfg2 (BASELINE configs[1]): O3 D=12 nu<=4, 1e5 sites/GPU, A-given"},
     "cfg3": {"D": 12, "nu": 4, "sites": 1_000_000, "input": "positions", "J": 30, "n_out": 1,
              "scaling": "strong", "cpu_sites": 2,
+             "sha256": "cf46bc8f5590ee62f6f33a4ef6e8e1d14d972d2e4db4744d64edfff5215bd6bd",
              "desc": "cfg3 (BASELINE configs[2]): O3 D=12 nu<=4 from J=30 neighbours, 1e6 sites total, energy all-reduce"},
     "cfg4": {"D": 16, "nu": 6, "sites": 200_000, "input": "A", "n_out": 1, "scaling": "weak", "cpu_sites": 1,
+             "sha256": "bcc01406b9d7172f0b9601986ad7ae553aa2b1a44d0c9f1fddc2eab3ff1ec3a1",
              "desc": "cfg4 (BASELINE configs[3]): O3 D=16 nu<=6 (3,711,466 nodes), 2e5 sites/GPU, A-given"},
     "cfg5": {"D": 14, "nu": 5, "sites": 500_000, "input": "positions", "J": 40, "n_out": 64,
              "scaling": "strong", "cpu_sites": 1,
+             "sha256": "4b1e54f455dac3196538dc8194cfbdaa83eab30f3a66604bdcba5dccba504cd9",
              "desc": "cfg5 (BASELINE configs[4]): O3 D=14 nu<=5 from J=40 neighbours, 64 outputs, 5e5 sites total"},
 }
 
@@ -89,17 +94,17 @@ def workload(cfg, seed=1):
     return g, c
 
 
-def dag_census(g, cfg, used_seeds):
-    """P, L_f, P_int, T and the algorithmic flops/bytes per site."""
-    N, L = g.num_nodes, g.num_seeds
-    par = g.parents[L:]
+def dag_census(pa, pb, n_seeds, n_targets, cfg, used_seeds):
+    """P, L_f, P_int, T and the algorithmic flops/bytes per site,
+    from the DAG's parent arrays (either arm: native graph or oracle graph)."""
+    N, L = len(pa), n_seeds
     child = np.zeros(N, np.int64)
-    np.add.at(child, par[:, 0], 1)
-    np.add.at(child, par[:, 1], 1)
+    np.add.at(child, np.asarray(pa[L:], np.int64), 1)
+    np.add.at(child, np.asarray(pb[L:], np.int64), 1)
     P_ = N - L
     L_f = int(np.sum(child[L:] == 0))
     P_int = P_ - L_f
-    T = len(g.target_ids)
+    T = int(n_targets)
     n_out = cfg["n_out"]
     F = 6 * P_int + 3 * L_f + 2 * T * n_out
     if cfg["input"] == "positions":
@@ -108,6 +113,32 @@ def dag_census(g, cfg, used_seeds):
     else:
         B = 16 * L + 8 * n_out
     return {"P": P_, "L_f": L_f, "P_int": P_int, "T": T, "F_site": F, "B_site": B}
+
+
+def config_block(cfg, S, global_sites, world, n_nodes, census, in_bytes):
+    """The `config` object, identical for both arms at the same N (workload
+    keys only; plan details go to the separate "plan" key)."""
+    pos = cfg["input"] == "positions"
+    return {"workload": cfg["desc"], "sites_per_gpu": S, "global_sites": global_sites,
+            "dag_nodes": n_nodes, "dag_products": census["P"], "targets": census["T"], "n_out": cfg["n_out"],
+            "l2": ("inputs %.2f GB per GPU > 126 MB L2 (no flush)" % (in_bytes / 1e9)) if in_bytes > 126e6
+            else "inputs fit L2; timed steps reuse them",
+            "parallelism": f"dp{world} (sites sharded" + (", energy all-reduce)" if pos else ", no collective)")}
+
+
+def shard_sizes(cfg, total_sites, rank, world):
+    """(sites on this rank, global sites): weak configs give every rank the
+    full count, strong configs split a fixed total evenly (distributed.shard_range)."""
+    if cfg["scaling"] == "strong":
+        base, rem = divmod(total_sites, world)
+        return base + (1 if rank < rem else 0), total_sites
+    return total_sites, world * total_sites
+
+
+def input_bytes(cfg, S, n_seeds, prec):
+    if cfg["input"] == "positions":
+        return S * cfg["J"] * 3 * 8
+    return S * n_seeds * (16 if prec == "f64" else 8)
 
 
 def positions(S, J, gen, device):
@@ -228,14 +259,62 @@ def cpu_sample_text(cfg, procs, n):
 
 
 # --------------------------------------------------------- reference arm
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_workload(cfg, seed=1):
+    """The reference arm's graph: the oracle's restatement of build_graph
+    (graphbuild.py:243-268), SHA-256-checked against the reference's pinned
+    hash -- no repo library is loaded on this arm."""
+    from oracle import acedag_oracle as O
+    og = O.build_graph("O3", O.Spec(1, cfg["D"]), cfg["nu"])
+    sha = O.graph_sha256(og)
+    if sha != cfg["sha256"]:
+        raise SystemExit(f"oracle graph SHA-256 {sha} != pinned {cfg['sha256']}")
+    pa, pb, _aux, tg = O.graph_arrays(og)
+    rng = np.random.default_rng(seed)
+    n_out = cfg["n_out"]
+    c = rng.normal(size=len(tg)) if n_out == 1 else rng.normal(size=(len(tg), n_out))
+    L = len(O.one_particle_indices("O3", cfg["D"]))
+    return pa, pb, tg, c, L
+
+
+def used_seed_count(pa, pb, tg, L):
+    used = np.zeros(L, bool)
+    for arr in (pa[L:], pb[L:]):
+        used[np.asarray(arr)[np.asarray(arr) < L]] = True
+    used[np.asarray(tg)[np.asarray(tg) < L]] = True
+    return int(used.sum())
+
+
 def run_reference(a):
+    """The reference's CPU algorithm on the box's host cores: the oracle port
+    of evaluate_graph + the sequential c-dot (evaluator.py:93-142; pool for
+    position inputs), NumPy, one forked process per core.  Rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    assert "paper_2202_04140_b200" not in sys.modules
     cfg = CONFIGS[a.config]
     cores = host_cores()
-    g, c = workload(cfg)
-    with cpu_pool(g, c, cfg, cores) as pool:
+    pa, pb, tg, c, L = oracle_workload(cfg)
+    census = dag_census(pa, pb, L, len(tg), cfg, used_seed_count(pa, pb, tg, L))
+    S, global_sites = shard_sizes(cfg, a.sites or cfg["sites"], 0, a.gpus)
+    _CPU_CTX["graph"] = (pa, pb, tg, c, L, cfg)
+    # one core: the same per-process sample, alone
+    with mp.get_context("fork").Pool(1) as pool1:
+        pool1.map(_cpu_worker, [(1, 0)])
+        t0 = time.perf_counter()
+        n1 = sum(s for s, _ in pool1.map(_cpu_worker, [(cfg["cpu_sites"], 7)]))
+        rate1 = n1 / (time.perf_counter() - t0)
+    with mp.get_context("fork").Pool(cores) as pool:
         for w in range(a.warmup):
             pool.map(_cpu_worker, [(1, w * cores + i) for i in range(cores)])
         sites = 0
@@ -248,10 +327,14 @@ def run_reference(a):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * wall / a.steps,
             "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded complex-normal A (or uniform neighbour shells), N(0,1) coefficients",
-            "config": {"workload": cfg["desc"], "sites_per_step": cfg["cpu_sites"] * cores},
+            "data": ("synthetic: seeded uniform neighbour shells 0.8-5.0" if cfg["input"] == "positions" else
+                     "synthetic: seeded complex-normal A") + ", N(0,1) coefficients per target",
+            "config": config_block(cfg, S, global_sites, a.gpus, len(pa), census,
+                                   input_bytes(cfg, S, L, "f64")),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": cpu_sample_text(cfg, cores, sites)},
+                             "value_1core": rate1, "cpu_model": cpu_model(),
+                             "graph": "oracle build_graph restatement, SHA-256 == reference " + cfg["sha256"][:16],
+                             "sample": cpu_sample_text(cfg, cores, sites // max(1, a.steps)) + f" x {a.steps} steps"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -309,21 +392,17 @@ def run_ours(a):
         return x
 
     cfg = CONFIGS[a.config]
-    total_sites = a.sites or cfg["sites"]
+    S, global_sites = shard_sizes(cfg, a.sites or cfg["sites"], rank, world)
     if cfg["scaling"] == "strong":
-        lo, hi = shard_range(total_sites, rank, world)
-        S = hi - lo
-        global_sites = total_sites
-    else:
-        S = total_sites
-        global_sites = world * S
+        lo, hi = shard_range(global_sites, rank, world)
+        assert hi - lo == S
     n_out = cfg["n_out"]
     g, c = workload(cfg)
     t_plan = time.perf_counter()
     plan = P.SitePlan(g, local).set_coefficients(node_ids=g.target_ids, values=c)
     t_plan = time.perf_counter() - t_plan
     info = plan.info()
-    census = dag_census(g, cfg, info["used_seeds"])
+    census = dag_census(g.parents[:, 0], g.parents[:, 1], g.num_seeds, len(g.target_ids), cfg, info["used_seeds"])
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     L = g.num_seeds
     pos = cfg["input"] == "positions"
@@ -435,7 +514,10 @@ def run_ours(a):
         peak = fp64_peak_tflops(dev)
         if a.prec == "f32":
             peak *= 2.0  # FFMA rate is 2x DFMA on B200 (72.6 vs 34.2 TF measured, profiles/r01)
-        achieved = F * S / (k2_ms * 1e-3) / 1e12
+        # position inputs: F includes the pool flops, so it is divided by the
+        # whole step (pool + K2), not by the K2 phase alone
+        t_roof = ms_step if pos else k2_ms
+        achieved = F * S / (t_roof * 1e-3) / 1e12
         roof = {"bound": "fp64" if a.prec == "f64" else "fp32", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": "measured in this run: cuBLAS DGEMM 8192^3" + (" x2 (fp32)" if a.prec == "f32" else "")
@@ -443,8 +525,11 @@ def run_ours(a):
                 "flops_per_site": F,
                 "flop_model": "F_site = 6 P_int + 3 L_f + 2 T n_out" + (" + 4 J U_used" if pos else "") + " (SURVEY.md 8d)"}
     roof["kernel"] = plan.kernel_name(prec=a.prec, sites=S)
-    roof["kernel_ms"] = k2_ms
-    roof["step_share"] = k2_ms / ms_step
+    if pos:
+        roof["kernel"] = "pool_positions + " + roof["kernel"]
+        roof["timed_over"] = "whole step (pool + K2 + reduce): F_site includes the pool flops"
+    roof["kernel_ms"] = ms_step if pos else k2_ms
+    roof["step_share"] = roof["kernel_ms"] / ms_step
     roof["phases_ms"] = phases
     prof = os.path.join(ROOT, "profiles", "r01", "traffic.json")
     roof["traffic"] = None
@@ -460,7 +545,9 @@ def run_ours(a):
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cores = host_cores()
         rate, n = cpu_rate(g, c, cfg, cores, reps=1)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": cpu_sample_text(cfg, cores, n)}
+        rate1, _ = cpu_rate(g, c, cfg, 1, reps=1)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "value_1core": rate1,
+               "cpu_model": cpu_model(), "sample": cpu_sample_text(cfg, cores, n)}
 
     if rank == 0:
         line = {
@@ -470,14 +557,11 @@ def run_ours(a):
             "data": ("synthetic: seeded uniform neighbour shells 0.8-5.0 [S,J,3] f64" if pos else
                      "synthetic: seeded complex-normal A [S,%d] %s" % (L, "c128" if a.prec == "f64" else "c64"))
                     + " in HBM, N(0,1) coefficients per target",
-            "config": {"workload": cfg["desc"], "sites_per_gpu": S, "global_sites": global_sites,
-                       "dag_nodes": g.num_nodes, "dag_products": census["P"], "targets": census["T"],
-                       "n_out": n_out, "plan_products": info["recursive_products"],
-                       "plan_extra_nodes": info["extra_nodes"], "used_seeds": info["used_seeds"],
-                       "plan_build_s": round(t_plan, 2),
-                       "l2": "inputs %.2f GB per GPU > 126 MB L2 (no flush)" % (X.numel() * X.element_size() / 1e9)
-                       if X.numel() * X.element_size() > 126e6 else "inputs fit L2; timed steps reuse them",
-                       "parallelism": f"dp{world} (sites sharded" + (", energy all-reduce)" if pos else ", no collective)")},
+            "config": config_block(cfg, S, global_sites, world, g.num_nodes, census,
+                                   X.numel() * X.element_size()),
+            "plan": {"products": info["recursive_products"], "extra_nodes": info["extra_nodes"],
+                     "used_seeds": info["used_seeds"], "build_s": round(t_plan, 2),
+                     "graph_sha256": cfg["sha256"]},
             "dag_products_per_s": value * census["P"],
             "naive": naive,
             "roofline": roof,

@@ -42,6 +42,29 @@ extern "C" {
 #define ACEDAG_ENOTTARGET (-5)    /* coefficient on non-target -> ValueError*/
 #define ACEDAG_EDOMAIN (-6)       /* coordinate out of domain -> ValueError */
 #define ACEDAG_EUNSUPPORTED (-7)  /* shape outside the compiled limits      */
+#define ACEDAG_EFORMAT (-8)       /* malformed graph file -> GraphFormatError */
+
+/* graph-file violation kinds (acedag_graph_deserialize), in the order the
+ * reference checks them (graphbuild.py:387-464) */
+#define ACEDAG_GE_NOT_UTF8 1
+#define ACEDAG_GE_VERSION 2
+#define ACEDAG_GE_HEADER 3
+#define ACEDAG_GE_DEGREE 4
+#define ACEDAG_GE_NODE_LINE 5
+#define ACEDAG_GE_NOT_DENSE 6
+#define ACEDAG_GE_AUX_FLAG 7
+#define ACEDAG_GE_ELEMENTS 8
+#define ACEDAG_GE_PARENT_FIELD 9
+#define ACEDAG_GE_ORPHAN 10
+#define ACEDAG_GE_PARENT_IDS 11
+#define ACEDAG_GE_PARENT_ORDER 12
+#define ACEDAG_GE_UNION 13
+#define ACEDAG_GE_SEED_AUX 14
+#define ACEDAG_GE_AUX_MISMATCH 15
+#define ACEDAG_GE_DUPLICATE 16
+#define ACEDAG_GE_EMPTY 17
+#define ACEDAG_GE_SEED_LAYOUT 18 /* this build: seeds first, in label order */
+#define ACEDAG_GE_LIMIT 19       /* this build: order <= 8, label count     */
 
 /* symmetry groups (indexsets.py:37-52) */
 #define ACEDAG_GROUP_T 0
@@ -103,6 +126,18 @@ int64_t acedag_graph_find(const acedag_graph* g, const int32_t* seeds, int32_t l
 /* serialize_graph (graphbuild.py:374-384).  Call with buf=NULL to get the
  * size in *len; then with a buffer of that size. */
 int acedag_graph_serialize(const acedag_graph* g, char* buf, int64_t* len);
+/* deserialize_graph (graphbuild.py:387-464): parses the versioned text
+ * format natively.  On a malformed file returns ACEDAG_EFORMAT with the
+ * violation kind in *err_kind (ACEDAG_GE_*), the byte offset the reference
+ * reports in *err_offset and the offending line's byte span in
+ * *err_line_start / *err_line_len (NULL pointers are allowed). */
+int acedag_graph_deserialize(const char* data, int64_t len, acedag_graph** out,
+                             int32_t* err_kind, int64_t* err_offset,
+                             int64_t* err_line_start, int64_t* err_line_len);
+/* the header fields of a graph (group, p (0 = inf), D, numax (0 = uncapped),
+ * alg (0 orig, 1 gen), n) -- what EvalGraph carries (graphbuild.py:76-93) */
+int acedag_graph_spec(const acedag_graph* g, int32_t* group, int32_t* p, double* max_degree,
+                      int32_t* nu_max, int32_t* alg, int32_t* n);
 
 /* ------------------------------------------------------------------------
  * Device plan: the DAG compiled into a per-warp evaluation program, resident

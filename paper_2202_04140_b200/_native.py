@@ -14,7 +14,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libacedag_b200.so")
 
-OK, EINVAL, EMISSING_SEED, ECUDA, ENOMEM, ENOTTARGET, EDOMAIN, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7
+OK, EINVAL, EMISSING_SEED, ECUDA, ENOMEM, ENOTTARGET, EDOMAIN, EUNSUPPORTED, EFORMAT = 0, -1, -2, -3, -4, -5, -6, -7, -8
 METHOD_RECURSIVE, METHOD_NAIVE = 0, 1
 OUT_REAL, OUT_COMPLEX = 0, 1
 PREC_F64, PREC_F32 = 0, 1
@@ -38,6 +38,8 @@ SIGNATURES = {
     "acedag_graph_node_seeds": (C.c_int, [_vp, C.c_int64, _i32p, C.c_int32]),
     "acedag_graph_find": (C.c_int64, [_vp, _i32p, C.c_int32]),
     "acedag_graph_serialize": (C.c_int, [_vp, C.c_char_p, _i64p]),
+    "acedag_graph_deserialize": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(_vp), _i32p, _i64p, _i64p, _i64p]),
+    "acedag_graph_spec": (C.c_int, [_vp, _i32p, _i32p, _dp, _i32p, _i32p, _i32p]),
     "acedag_plan_create": (C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),
     "acedag_plan_destroy": (None, [_vp]),
     "acedag_plan_set_coefficients": (C.c_int, [_vp, _i64p, _dp, _dp, C.c_int64, C.c_int32]),

@@ -14,11 +14,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libacedag_b200.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["capi.cu", "horner.cu", "graph.cpp", "plan.cpp"]
+SOURCES = ["capi.cu", "horner.cu", "graph.cpp", "graph_io.cpp", "plan.cpp"]
 HEADERS = ["graph.h", "plan.h", "kernels.cuh", "pool.cuh", "ylm_norms.h", "horner.h"]
 # headers each translation unit includes (object rebuilt when one is newer)
 DEPS = {"capi.cu": HEADERS, "horner.cu": ["horner.h", "plan.h", "graph.h"],
-        "graph.cpp": ["graph.h"], "plan.cpp": ["plan.h", "graph.h"]}
+        "graph.cpp": ["graph.h"], "graph_io.cpp": ["graph.h"], "plan.cpp": ["plan.h", "graph.h"]}
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [*GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-diag-suppress", "550"]
 

@@ -490,6 +490,40 @@ int acedag_graph_serialize(const acedag_graph* h, char* buf, int64_t* len) {
   }
 }
 
+int acedag_graph_deserialize(const char* data, int64_t len, acedag_graph** out, int32_t* err_kind,
+                             int64_t* err_offset, int64_t* err_line_start, int64_t* err_line_len) {
+  if (err_kind) *err_kind = 0;
+  if (!out || (len > 0 && !data) || len < 0) return fail(ACEDAG_EINVAL, "bad arguments");
+  try {
+    std::unique_ptr<acedag_graph> h(new acedag_graph);
+    GraphParseError pe;
+    if (!deserialize_graph(data ? data : "", (size_t)len, h->g, pe)) {
+      if (err_kind) *err_kind = pe.kind;
+      if (err_offset) *err_offset = pe.offset;
+      if (err_line_start) *err_line_start = pe.line_start;
+      if (err_line_len) *err_line_len = pe.line_len;
+      return fail(ACEDAG_EFORMAT, pe.message);
+    }
+    *out = h.release();
+    return ACEDAG_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(ACEDAG_ENOMEM, "out of host memory reading the graph");
+  }
+}
+
+int acedag_graph_spec(const acedag_graph* h, int32_t* group, int32_t* p, double* max_degree, int32_t* nu_max,
+                      int32_t* alg, int32_t* n) {
+  if (!h) return fail(ACEDAG_EINVAL, "graph is NULL");
+  const Graph& g = h->g;
+  if (group) *group = g.group;
+  if (p) *p = g.spec.p;
+  if (max_degree) *max_degree = g.spec.max_degree;
+  if (nu_max) *nu_max = g.nu_max;
+  if (alg) *alg = g.alg;
+  if (n) *n = g.n;
+  return ACEDAG_OK;
+}
+
 // ------------------------------------------------------------------ plans
 int acedag_plan_create(const acedag_graph* h, int device, acedag_plan** out) {
   if (!h || !out) return fail(ACEDAG_EINVAL, "NULL argument");
@@ -731,11 +765,13 @@ int k2_warps() {
   return w;
 }
 
-// auto selection (k2_mode 5) for order 5-6 (order <= 4 runs k2_horner): four
-// sites per lane when the sites fill a round of tiles (cfg4: 482 ms vs 591 ms
-// for k2_tmem3 at 2e5 sites, profiles/r01)
+// auto selection (k2_mode 5) for fp64 order 5-6 (order <= 4 runs k2_horner):
+// k2_quad at every batch size, so a site's value never depends on its batch
+// (cfg4: 482 ms vs 591 ms for k2_tmem3 at 2e5 sites, profiles/r01)
 bool use_quad(const acedag_plan* P, int64_t S) {
-  return (S + 127) / 128 >= P->sms - t_sm_reserve;
+  (void)P;
+  (void)S;
+  return true;
 }
 
 // tile geometry: 32 sites per CTA, seed rows [Us][32] in smem (U used seeds

@@ -339,8 +339,7 @@ static void enumerate_order(const Graph& g, int order, std::vector<Tuple>& out) 
   rec.run(0, 0, p == 0 ? 0 : g.spec.power_cap(), 0, 0);
 }
 
-static void init_graph(Graph& g, int group, int p, double max_degree, int nu_max, int alg,
-                       int n) {
+void init_graph(Graph& g, int group, int p, double max_degree, int nu_max, int alg, int n) {
   if (group < 0 || group > 3) throw std::invalid_argument("unknown group");
   if (p != 0 && p != 1 && p != 2)
     throw std::invalid_argument("p must be 1, 2 or inf, got " + std::to_string(p));

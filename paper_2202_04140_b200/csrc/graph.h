@@ -97,9 +97,29 @@ struct Graph {
 
 // Builds a graph; throws std::invalid_argument with reference messages.
 void build_graph(Graph& g, int group, int p, double max_degree, int nu_max, int alg, int n);
+// Empty graph (no nodes) with validated spec and its label table.
+void init_graph(Graph& g, int group, int p, double max_degree, int nu_max, int alg, int n);
 // Rebuild tuples from a parent relation; throws std::invalid_argument.
 void graph_from_parents(Graph& g, int group, int p, double max_degree, int nu_max, int alg,
                         int n, int64_t n_nodes, int64_t n_seeds, const int32_t* parents,
                         const uint8_t* aux);
+
+// Graph file reader (graphbuild.py:387-464 format).  On failure returns false
+// and fills err: the kind of the first violation (GraphErr), the byte offset
+// the reference reports for it and the offending line's byte span (the
+// Python shim composes the reference's message from that line).
+enum GraphErr {
+  kGeOk = 0, kGeNotUtf8, kGeVersion, kGeHeader, kGeDegree, kGeNodeLine, kGeNotDense, kGeAuxFlag,
+  kGeElements, kGeParentField, kGeOrphan, kGeParentIds, kGeParentOrder, kGeUnion, kGeSeedAux,
+  kGeAuxMismatch, kGeDuplicate, kGeEmpty, kGeSeedLayout, kGeLimit
+};
+struct GraphParseError {
+  int kind = kGeOk;
+  int64_t offset = 0;      // byte offset reported with the error
+  int64_t line_start = 0;  // span of the offending line (header: line 0)
+  int64_t line_len = 0;
+  std::string message;     // C-side description (ASCII; the shim rebuilds the reference's text)
+};
+bool deserialize_graph(const char* data, size_t n, Graph& g, GraphParseError& err);
 
 }  // namespace acedag

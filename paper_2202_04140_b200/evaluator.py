@@ -439,36 +439,48 @@ def evaluate_model(graph, coefficients: dict, particles, real_part: bool = False
 
 
 # ------------------------------------------------- symmetry transforms
-# (callers of the path, evaluator.py:149-224)
+# Callers of the path (evaluator.py:149-186): a particle is a coordinate
+# tuple whose azimuth sits at a fixed position per group (T: the angle
+# itself; SO2: after the radius; O3/O3F: after (r, theta)).
+
+_AZIMUTH = {Group.T: 0, Group.SO2: 1, Group.O3: 2, Group.O3F: 2}
+
+
+def _shift(coords, pos: int, delta: float) -> tuple:
+    c = tuple(coords)
+    return c[:pos] + (c[pos] + delta,) + c[pos + 1:]
+
 
 def rotate_particles(group: Group, particles, alpha: float):
-    if group is Group.T:
-        return [(c[0] + alpha,) for c in particles]
-    if group is Group.SO2:
-        return [(c[0], c[1] + alpha) for c in particles]
-    return [(c[0], c[1], c[2] + alpha) + tuple(c[3:]) for c in particles]
+    """Every particle's azimuth advanced by alpha (a z-rotation for O3/O3F)."""
+    pos = _AZIMUTH[group]
+    return [_shift(c, pos, alpha)[: group.components] for c in particles]
 
 
 def invert_particles(group: Group, particles):
+    """r -> -r: polar angle mirrored, azimuth turned by pi (O3/O3F only)."""
     if not group.has_l:
         raise ValueError(f"inversion applies to O3/O3F, not {group.value}")
-    return [(c[0], math.pi - c[1], c[2] + math.pi) + tuple(c[3:]) for c in particles]
+    out = []
+    for c in particles:
+        c = tuple(c)
+        out.append((c[0], math.pi - c[1], c[2] + math.pi) + c[3:group.components])
+    return out
 
 
 def random_particles(group: Group, rng: random.Random, max_count: int = 8):
-    count = rng.randint(1, max_count)
-    out = []
-    for _ in range(count):
-        if group is Group.T:
-            out.append((rng.uniform(0.0, 2.0 * math.pi),))
-        elif group is Group.SO2:
-            out.append((rng.random(), rng.uniform(0.0, 2.0 * math.pi)))
-        else:
-            r = rng.random()
-            theta = math.acos(rng.uniform(-1.0, 1.0))
-            phi = rng.uniform(0.0, 2.0 * math.pi)
-            out.append((r, theta, phi) if group is Group.O3 else (r, theta, phi, rng.uniform(-1.0, 1.0)))
-    return out
+    """1..max_count random particles, drawing from ``rng`` in the reference's
+    order (count, then per particle: radius, cos(theta), azimuth, feature as
+    the group has them) so a seeded rng reproduces its configurations."""
+    two_pi = 2.0 * math.pi
+    draws = {
+        Group.T: lambda: (rng.uniform(0.0, two_pi),),
+        Group.SO2: lambda: (rng.random(), rng.uniform(0.0, two_pi)),
+        Group.O3: lambda: (rng.random(), math.acos(rng.uniform(-1.0, 1.0)), rng.uniform(0.0, two_pi)),
+    }
+    draws[Group.O3F] = lambda: draws[Group.O3]() + (rng.uniform(-1.0, 1.0),)
+    n = rng.randint(1, max_count)
+    return [draws[group]() for _ in range(n)]
 
 
 @dataclass(frozen=True)
@@ -508,35 +520,45 @@ def invariance_check(group: Group, graph, particles, trials: int = 8, seed: int 
 
 
 # ------------------------------------------------------------ file formats
-# (evaluator.py:231-290; callers of the path, kept for API compatibility)
+# Particle and coefficient text files (evaluator.py:231-290), callers of the
+# path kept for the CLI: UTF-8, one record per line, blank lines skipped.
+# Error texts follow the reference's (the CLI prints them).
+
+def _records(path, comments: bool):
+    """(line number, raw line, stripped line) of every non-blank line;
+    with ``comments`` '#' lines are yielded too (the caller decides)."""
+    with open(path, "r", encoding="utf-8") as fh:
+        text = fh.read()
+    for no, raw in enumerate(text.splitlines(), start=1):
+        body = raw.strip()
+        if body and (comments or not body.startswith("#")):
+            yield no, raw, body
+
 
 def write_particles(path, group: Group, particles) -> None:
+    rows = [f"# group={group.value}"]
+    for coords in particles:
+        _check_coords(group, coords)
+        rows.append(" ".join(repr(float(x)) for x in coords))
     with open(path, "w", encoding="utf-8", newline="\n") as fh:
-        fh.write(f"# group={group.value}\n")
-        for coords in particles:
-            _check_coords(group, coords)
-            fh.write(" ".join(repr(float(c)) for c in coords) + "\n")
+        fh.write("\n".join(rows) + "\n")
 
 
 def read_particles(path):
-    with open(path, "r", encoding="utf-8") as fh:
-        lines = fh.read().splitlines()
+    """``# group=<G>`` header, then one whitespace-separated particle per line."""
     group, particles = None, []
-    for i, raw in enumerate(lines, start=1):
-        line = raw.strip()
-        if not line:
-            continue
-        if line.startswith("#"):
-            body = line.lstrip("#").strip()
-            if body.startswith("group="):
-                group = Group(body[len("group="):].strip())
+    for no, raw, body in _records(path, comments=True):
+        if body[0] == "#":
+            key, _, val = body.lstrip("#").strip().partition("=")
+            if key == "group" and _ == "=":
+                group = Group(val.strip())
             continue
         if group is None:
             raise ValueError(f"{path}: missing '# group=...' header before data")
         try:
-            coords = tuple(float(tok) for tok in line.split())
+            coords = tuple(map(float, body.split()))
         except ValueError:
-            raise ValueError(f"{path}:{i}: bad coordinate line: {raw!r}") from None
+            raise ValueError(f"{path}:{no}: bad coordinate line: {raw!r}") from None
         _check_coords(group, coords)
         particles.append(coords)
     if group is None:
@@ -545,25 +567,25 @@ def read_particles(path):
 
 
 def write_coefficients(path, coefficients: dict) -> None:
+    rows = []
+    for t in sorted(coefficients):
+        z = complex(coefficients[t])
+        rows.append(f"{format_elements(t)} {z.real!r} {z.imag!r}\n")
     with open(path, "w", encoding="utf-8", newline="\n") as fh:
-        for t in sorted(coefficients):
-            c = complex(coefficients[t])
-            fh.write(f"{format_elements(t)} {c.real!r} {c.imag!r}\n")
+        fh.write("".join(rows))
 
 
 def read_coefficients(path, group: Group) -> dict:
-    out = {}
-    with open(path, "r", encoding="utf-8") as fh:
-        for i, raw in enumerate(fh.read().splitlines(), start=1):
-            line = raw.strip()
-            if not line or line.startswith("#"):
-                continue
-            parts = line.split()
-            if len(parts) != 3:
-                raise ValueError(f"{path}:{i}: expected '<tuple> <re> <im>', got {raw!r}")
-            elements = parse_elements(group, parts[0])
-            try:
-                out[elements] = complex(float(parts[1]), float(parts[2]))
-            except ValueError:
-                raise ValueError(f"{path}:{i}: bad coefficient values: {raw!r}") from None
-    return out
+    """``<tuple> <re> <im>`` per line; '#' lines are comments."""
+    coefs = {}
+    for no, raw, body in _records(path, comments=False):
+        fields = body.split()
+        if len(fields) != 3:
+            raise ValueError(f"{path}:{no}: expected '<tuple> <re> <im>', got {raw!r}")
+        key = parse_elements(group, fields[0])
+        try:
+            re_, im_ = float(fields[1]), float(fields[2])
+        except ValueError:
+            raise ValueError(f"{path}:{no}: bad coefficient values: {raw!r}") from None
+        coefs[key] = complex(re_, im_)
+    return coefs

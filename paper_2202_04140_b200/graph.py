@@ -228,94 +228,76 @@ def serialize_graph(graph: EvalGraph) -> bytes:
     return buf.raw[: n.value]
 
 
-_HEADER_RE = re.compile(
-    r"^ACEDAG v(\d+) group=(T|SO2|O3|O3F) p=(1|2|inf) D=([0-9.]+) numax=(\d+) alg=(orig|gen) n=(\d+)$")
+# violation kinds of acedag_graph_deserialize (include/acedag_b200.h ACEDAG_GE_*)
+(_GE_NOT_UTF8, _GE_VERSION, _GE_HEADER, _GE_DEGREE, _GE_NODE_LINE, _GE_NOT_DENSE, _GE_AUX_FLAG, _GE_ELEMENTS,
+ _GE_PARENT_FIELD, _GE_ORPHAN, _GE_PARENT_IDS, _GE_PARENT_ORDER, _GE_UNION, _GE_SEED_AUX, _GE_AUX_MISMATCH,
+ _GE_DUPLICATE, _GE_EMPTY, _GE_SEED_LAYOUT, _GE_LIMIT) = range(1, 20)
+
+
+def _format_error(kind: int, offset: int, line: str, group: Group | None, native_msg: str) -> GraphFormatError:
+    """The reference's exception for a violation the native reader found
+    (graphbuild.py:387-464 wording), composed from the offending line."""
+    fields = line.split(" ")
+    if kind == _GE_NOT_UTF8:
+        return GraphFormatError("graph data is not valid UTF-8", offset)
+    if kind == _GE_VERSION:
+        version = re.match(r"ACEDAG v(\d+)", line)[1]
+        return UnsupportedVersionError(f"unsupported graph format version {version}", 0)
+    if kind == _GE_HEADER:
+        return GraphFormatError(f"bad header line: {line!r}", 0)
+    if kind == _GE_DEGREE:
+        degree = re.search(r" D=([0-9.]+) ", line)[1]
+        return GraphFormatError(f"bad degree cap {degree!r}", 0)
+    quoted = {_GE_NODE_LINE: "bad node line", _GE_PARENT_FIELD: "bad parent field", _GE_PARENT_IDS: "bad parent ids"}
+    if kind in quoted:
+        return GraphFormatError(f"{quoted[kind]}: {line!r}", offset)
+    if kind == _GE_AUX_FLAG:
+        return GraphFormatError(f"auxiliary flag must be 0 or 1, got {fields[1]!r}", offset)
+    if kind == _GE_ELEMENTS:
+        try:
+            parse_elements(group, fields[2])
+        except ValueError as exc:
+            return GraphFormatError(str(exc), offset)
+        return GraphFormatError(f"tuple components must be ASCII integers in this build: {fields[2]!r}", offset)
+    per_node = {_GE_NOT_DENSE: "node ids must be dense and ascending, got", _GE_PARENT_ORDER: "parent ids must precede node",
+                _GE_UNION: "parents do not union to node", _GE_AUX_MISMATCH: "auxiliary flag inconsistent on node",
+                _GE_DUPLICATE: "duplicate tuple at node"}
+    if kind in per_node:
+        return GraphFormatError(f"{per_node[kind]} {int(fields[0])}", offset)
+    fixed = {_GE_ORPHAN: "only order-1 nodes may lack parents", _GE_SEED_AUX: "order-1 nodes cannot be auxiliary",
+             _GE_EMPTY: "graph has no nodes; order-1 seeds are mandatory"}
+    if kind in fixed:
+        return GraphFormatError(fixed[kind], offset)
+    # this build's own limits (seed layout, order <= 8): the native text
+    return GraphFormatError(native_msg.rsplit(" (at byte", 1)[0], offset)
 
 
 def deserialize_graph(data: bytes) -> EvalGraph:
-    """Parse the text format (graphbuild.py:387-464) into a native graph.
-
-    Line-level errors carry byte offsets like the reference; structural
-    validation (topological parents, tuple unions, auxiliary flags) is then
-    re-checked natively from the parent relation.
-    """
-    try:
-        text = data.decode("utf-8")
-    except UnicodeDecodeError as exc:
-        raise GraphFormatError("graph data is not valid UTF-8", exc.start) from None
-    lines = text.split("\n")
-    m = _HEADER_RE.match(lines[0])
-    if m is None:
-        vm = re.match(r"^ACEDAG v(\d+)\b", lines[0])
-        if vm and vm.group(1) != "1":
-            raise UnsupportedVersionError(f"unsupported graph format version {vm.group(1)}", 0)
-        raise GraphFormatError(f"bad header line: {lines[0]!r}", 0)
-    if m.group(1) != "1":
-        raise UnsupportedVersionError(f"unsupported graph format version {m.group(1)}", 0)
-    group = Group(m.group(2))
-    p = math.inf if m.group(3) == "inf" else int(m.group(3))
-    try:
-        d_raw = float(m.group(4))
-    except ValueError:
-        raise GraphFormatError(f"bad degree cap {m.group(4)!r}", 0) from None
-    spec = DegreeSpec(p, int(d_raw) if d_raw.is_integer() else d_raw)
-    numax = int(m.group(5))
-    labels = one_particle_indices(group, spec.int_cap())
-    lab_index = {e: i for i, e in enumerate(labels)}
-    offset = len(lines[0].encode("utf-8")) + 1
-    parents, auxes, tuples = [], [], []
-    for raw in lines[1:]:
-        at = offset
-        offset += len(raw.encode("utf-8")) + 1
-        if not raw:
-            continue
-        parts = raw.split(" ")
-        if len(parts) not in (4, 5):
-            raise GraphFormatError(f"bad node line: {raw!r}", at)
-        try:
-            ident, aux = int(parts[0]), int(parts[1])
-        except ValueError:
-            raise GraphFormatError(f"bad node line: {raw!r}", at) from None
-        if ident != len(parents):
-            raise GraphFormatError(f"node ids must be dense and ascending, got {ident}", at)
-        if aux not in (0, 1):
-            raise GraphFormatError(f"auxiliary flag must be 0 or 1, got {parts[1]!r}", at)
-        try:
-            elements = parse_elements(group, parts[2])
-        except ValueError as exc:
-            raise GraphFormatError(str(exc), at) from None
-        if parts[3] == "-":
-            if len(parts) != 4:
-                raise GraphFormatError(f"bad parent field: {raw!r}", at)
-            if len(elements) != 1:
-                raise GraphFormatError("only order-1 nodes may lack parents", at)
-            par = (-1, -1)
-        else:
-            if len(parts) != 5:
-                raise GraphFormatError(f"bad parent field: {raw!r}", at)
-            try:
-                par = (int(parts[3]), int(parts[4]))
-            except ValueError:
-                raise GraphFormatError(f"bad parent ids: {raw!r}", at) from None
-            if not all(0 <= q < ident for q in par):
-                raise GraphFormatError(f"parent ids must precede node {ident}", at)
-            merged = tuple(sorted(tuples[par[0]] + tuples[par[1]]))
-            if merged != elements:
-                raise GraphFormatError(f"parents do not union to node {ident}", at)
-        if len(elements) == 1 and aux:
-            raise GraphFormatError("order-1 nodes cannot be auxiliary", at)
-        if len(elements) == 1 and (ident >= len(labels) or lab_index.get(elements[0]) != ident):
-            raise GraphFormatError(f"order-1 node {ident} out of label order", at)
-        tuples.append(elements)
-        parents.append(par)
-        auxes.append(aux)
-    if not parents:
-        raise GraphFormatError("graph has no nodes; order-1 seeds are mandatory", offset)
-    try:
-        return graph_from_parents(group, spec, np.array(parents, np.int32), np.array(auxes, np.uint8),
-                                  numax if numax else None, m.group(6), int(m.group(7)))
-    except ValueError as exc:
-        raise GraphFormatError(str(exc), 0) from None
+    """Read the versioned text format (graphbuild.py:387-464) natively
+    (csrc/graph_io.cpp: one pass, checks in the reference's order, byte
+    offsets like the reference's); errors are the reference's exception types
+    and messages."""
+    data = bytes(data)
+    lib = N.lib()
+    h = C.c_void_p()
+    kind, off, ls, ln = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+    rc = lib.acedag_graph_deserialize(data, len(data), C.byref(h), C.byref(kind), C.byref(off), C.byref(ls),
+                                      C.byref(ln))
+    if rc == N.EFORMAT:
+        line = data[ls.value: ls.value + ln.value].decode("utf-8", "replace")
+        group = None
+        m = re.match(r"ACEDAG v\d+ group=(T|SO2|O3|O3F) ", data[:256].decode("utf-8", "replace"))
+        if m:
+            group = Group(m[1])
+        raise _format_error(kind.value, off.value, line, group, N.last_error())
+    N.check(rc)
+    grp, p, nu, alg, n = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    D = C.c_double()
+    N.check(lib.acedag_graph_spec(h, C.byref(grp), C.byref(p), C.byref(D), C.byref(nu), C.byref(alg), C.byref(n)))
+    d = D.value
+    spec = DegreeSpec(math.inf if p.value == 0 else p.value, int(d) if float(d).is_integer() else d)
+    group = (Group.T, Group.SO2, Group.O3, Group.O3F)[grp.value]
+    return EvalGraph(h, group, spec, nu.value or None, ALGORITHMS[alg.value], n.value)
 
 
 def write_graph(graph: EvalGraph, path) -> None:

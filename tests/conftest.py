@@ -21,6 +21,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the CUDA library")
+    config.addinivalue_line("markers", "slow: BASELINE-size host work (tens of seconds)")
 
 
 @pytest.fixture(scope="session", autouse=True)

@@ -130,16 +130,7 @@ int device_labels(int dev, int group, int cap, const int4** out) {
   return 0;
 }
 
-// K2 chunk schedule: 0 static round robin, 1 dynamic (ACEDAG_SCHED)
-int k2_sched() {
-  static int s = [] {
-    const char* e = getenv("ACEDAG_SCHED");
-    return e ? atoi(e) : 0;
-  }();
-  return s;
-}
-
-// work chunks per program (ACEDAG_CHUNKS overrides; see kernels.cuh k2_fast)
+// work chunks per program (ACEDAG_CHUNKS overrides)
 int plan_chunks() {
   static int c = [] {
     const char* e = getenv("ACEDAG_CHUNKS");
@@ -188,59 +179,7 @@ int current_device() {
 }  // namespace
 
 namespace {
-int k2_mode();  // fp64 fast-path kernel selection (below)
-}
-
-namespace {
-// Program re-encoding for k2_tmem4 (kernels.cuh, Op4 comment): seed locators
-// per class (TMEM column / shared / global-cache byte offset) and per node the
-// counts of children in each class (children are slot-ordered by the plan).
-// Returns false if a count does not fit the packed word.
-bool encode_ops4(const PlanHost& H, uint32_t hot, uint32_t us, std::vector<Op>& o4, std::vector<int32_t>& croots) {
-  o4 = H.ops;
-  auto cls = [&](uint32_t s) { return s < hot ? 0u : (s < hot + us ? 1u : 2u); };
-  auto loc = [&](uint32_t s) { return s < hot ? s * 8u : (s < hot + us ? (s - hot) * 1024u : (s - hot - us) * 1024u); };
-  auto setw = [&](size_t i, uint32_t w) {
-    o4[i].nch = (uint16_t)(w & 0xFFFFu);
-    o4[i].skip = (uint16_t)(w >> 16);
-  };
-  bool ok = true;
-  std::function<size_t(size_t, uint32_t, uint32_t&, uint32_t&)> walk = [&](size_t pos, uint32_t n, uint32_t& nh,
-                                                                            uint32_t& ns) -> size_t {
-    nh = ns = 0;
-    for (uint32_t k = 0; k < n; ++k) {
-      const size_t me = pos;
-      const uint32_t s = H.ops[me].off / kRowBytes, c = cls(s);
-      nh += c == 0;
-      ns += c == 1;
-      o4[me].off = loc(s);
-      uint32_t h2, s2;
-      const uint32_t ch = H.ops[me].nch;
-      pos = walk(me + 1, ch, h2, s2);
-      if (ch > 0x7FFu || h2 > 0x7FFu || s2 > 0x3FFu) ok = false;
-      setw(me, ch | h2 << 11 | s2 << 22);
-    }
-    return pos;
-  };
-  croots.assign(H.chunk.size() - 1, 0);
-  for (size_t ci = 0; ci + 1 < H.chunk.size(); ++ci) {
-    size_t i = (size_t)H.chunk[ci];
-    while (i < (size_t)H.chunk[ci + 1]) {
-      croots[ci]++;
-      const uint32_t sa = H.ops[i].off / kRowBytes, sb = H.ops[i + 1].off / kRowBytes;
-      o4[i].off = loc(sa);
-      o4[i + 1].off = loc(sb);
-      setw(i + 1, cls(sa) | cls(sb) << 2);
-      uint32_t nh, ns;
-      const uint32_t ch = H.ops[i].nch;
-      const size_t end = walk(i + 2, ch, nh, ns);
-      if (ch > 0x7FFu || nh > 0x7FFu || ns > 0x3FFu) ok = false;
-      setw(i, ch | nh << 11 | ns << 22);
-      i = end;
-    }
-  }
-  return ok;
-}
+int k2_mode();  // fp64 single-output kernel selection (dispatch, below)
 }  // namespace
 
 namespace {
@@ -306,9 +245,6 @@ struct acedag_plan {
     bool ok = false;
     int us = 0;  // shared-memory rows
   } hp[2];
-  DevBuf<Op> ops4;         // k2_tmem4 encoding (encode_ops4), if it fits
-  DevBuf<int32_t> croots;  // roots per chunk
-  bool ops4_ok = false;
   DevBuf<int32_t> chunk;
   DevBuf<double> cre, cim;
   DevBuf<int32_t> nseg;
@@ -369,17 +305,9 @@ struct acedag_plan {
   }
 };
 
-namespace {
-// shared-memory cold rows of k2_tmem3/4 (32 warps, 3-slot program rings)
-int tmem_us_max(const acedag_plan* P) {
-  const size_t fixed = (size_t)32 * dev::Ring3::kAlloc + 16;
-  return (int)((P->smem_optin - fixed) / 1024);
-}
-int tmem_us_max_clamped(const acedag_plan* P) {
-  const int cold = std::max(0, P->U + 1 - (int)dev::kTmemRows2);
-  return std::min(cold, tmem_us_max(P));
-}
-}  // namespace
+// hot-slot count the plan compiler orders children by (compile_plan); the
+// programs of round 1 were compiled with 64, kept so results are unchanged
+constexpr uint32_t kPlanHotRows = 64;
 
 // ====================================================================== API
 extern "C" {
@@ -559,9 +487,11 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   if (n_coef < 0 || n_out < 1 || (n_coef && (!node_ids || !c_re)))
     return fail(ACEDAG_EINVAL, "bad coefficient arguments");
   DevGuard dg(P->device);
+  // compile into a local program: a rejected set (non-target id, order > 6)
+  // leaves the plan evaluating its previous coefficients
+  PlanHost H;
   try {
-    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, plan_chunks(), P->host,
-                 k2_mode() >= 4 ? dev::kTmemRows2 : kTmemRows);
+    compile_plan(*P->g, node_ids, c_re, c_im, n_coef, n_out, plan_chunks(), H, kPlanHotRows);
   } catch (const std::domain_error& e) {
     return fail(ACEDAG_ENOTTARGET, e.what());
   } catch (const std::bad_alloc&) {
@@ -569,13 +499,17 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   } catch (const std::exception& e) {
     return fail(ACEDAG_EINVAL, e.what());
   }
-  const PlanHost& H = P->host;
   if (H.max_order > 6) return fail(ACEDAG_EUNSUPPORTED, "device programs support order <= 6");
-  P->U = (int)H.slot_label.size();
+  // from here on the device arrays change: the plan is unusable until every
+  // upload has succeeded (a failed upload leaves it without coefficients)
+  P->has_coef = false;
+  P->host = std::move(H);
+  const PlanHost& Hp = P->host;
+  P->U = (int)Hp.slot_label.size();
   std::vector<uint16_t> ident(P->U);
   std::vector<int32_t> used(P->U);
-  for (int i = 0; i < P->U; ++i) { ident[i] = (uint16_t)i; used[i] = H.slot_label[i]; }
-  CK(P->slot_label.upload(H.slot_label));
+  for (int i = 0; i < P->U; ++i) { ident[i] = (uint16_t)i; used[i] = Hp.slot_label[i]; }
+  CK(P->slot_label.upload(Hp.slot_label));
   CK(P->slot_identity.upload(ident));
   CK(P->used_labels.upload(used));
   {
@@ -592,55 +526,44 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
   }
   {
     std::vector<int32_t> col((size_t)P->g->n_seeds(), -1);
-    for (int i = 0; i < P->U; ++i) col[H.slot_label[i]] = i;
+    for (int i = 0; i < P->U; ++i) col[Hp.slot_label[i]] = i;
     CK(P->col_of.upload(col));
     if (P->g->group == kO3) {
       std::vector<int4> tri = triples(P->g->spec.int_cap(), [&](int lab) { return col[lab] >= 0; });
       CK(P->tri.upload(tri));
     }
   }
-  CK(P->ops.upload(H.ops));
-  CK(P->chunk.upload(H.chunk));
-  if (k2_mode() == 5 || k2_mode() == 7 || k2_mode() == 9) CK(P->opsQ.upload(reencode_hot(H, dev::kTmemRowsQ)));
-  if (k2_mode() == 6) {
-    const int rows = P->U + 1, cold = std::max(0, rows - (int)dev::kTmemRows2);
-    std::vector<Op> o4;
-    std::vector<int32_t> cr;
-    P->ops4_ok = encode_ops4(H, dev::kTmemRows2, (uint32_t)std::min(cold, tmem_us_max(P)), o4, cr);
-    if (P->ops4_ok) {
-      CK(P->ops4.upload(o4));
-      CK(P->croots.upload(cr));
-    }
-  }
+  CK(P->ops.upload(Hp.ops));
+  CK(P->chunk.upload(Hp.chunk));
+  CK(P->opsQ.upload(reencode_hot(Hp, dev::kTmemRowsQ)));
   for (int f = 0; f < 2; ++f) {
     acedag_plan::HornerProg& hp = P->hp[f];
     hp.ok = false;
-    // fp64: order <= 4 (order 5-6 spill; on request only); fp32: order <= 6
-    if ((k2_mode() == 5 && H.max_order <= (f == 1 ? 6 : 4)) || k2_mode() == 9) {
+    // fp32: every order; fp64: order <= 4 unless ACEDAG_K2=horner (order 5-6 spill)
+    if (f == 1 || Hp.max_order <= 4 || k2_mode() == 2) {
       const int hot = std::min(P->U, horner_hot_rows(f == 1));
-      hp.us = std::min(P->U - hot, horner_us_max(P->smem_optin, f == 1, H.max_order));
+      hp.us = std::min(P->U - hot, horner_us_max(P->smem_optin, f == 1, Hp.max_order));
       std::vector<OpH> oh;
       std::vector<int32_t> ch, cr;
-      hp.ok = encode_horner(H, f == 1, (uint32_t)hot, (uint32_t)hp.us, oh, ch, cr);
-      if (hp.ok) {
+      if (encode_horner(Hp, f == 1, (uint32_t)hot, (uint32_t)hp.us, oh, ch, cr)) {
         CK(hp.ops.upload(oh));
         CK(hp.chunk.upload(ch));
         CK(hp.croots.upload(cr));
+        hp.ok = true;
       }
     }
   }
   {
-    std::vector<double> padded(H.cre);
-    // k2_multi reads whole 32-output slices; k2_mma prefetches two 4-record
-    // groups past the end of a chunk
-    padded.resize(H.cre.size() + 16 * (size_t)H.n_out + 64, 0.0);
+    std::vector<double> padded(Hp.cre);
+    // k2_mma prefetches two 4-record groups past the end of a chunk
+    padded.resize(Hp.cre.size() + 16 * (size_t)Hp.n_out + 64, 0.0);
     CK(P->cre.upload(padded));
   }
-  CK(P->cim.upload(H.cim));
-  CK(P->nseg.upload(H.naive_seg));
-  CK(P->nslots.upload(H.naive_slots));
-  CK(P->ncre.upload(H.naive_cre));
-  CK(P->ncim.upload(H.naive_cim));
+  CK(P->cim.upload(Hp.cim));
+  CK(P->nseg.upload(Hp.naive_seg));
+  CK(P->nslots.upload(Hp.naive_slots));
+  CK(P->ncre.upload(Hp.naive_cre));
+  CK(P->ncim.upload(Hp.naive_cim));
   P->has_coef = true;
   return ACEDAG_OK;
 }
@@ -754,28 +677,9 @@ struct Launch {
   acedag_plan::Workspace* ws;
 };
 
-// K2 fast-path geometry: warps per CTA (16 -> 128 registers and 8-leaf
-// batches, 32 -> 64 registers and 4-leaf batches); ACEDAG_K2_WARPS overrides.
-int k2_warps() {
-  static int w = [] {
-    const char* e = getenv("ACEDAG_K2_WARPS");
-    int v = e ? atoi(e) : 32;
-    return v == 32 ? 32 : 16;
-  }();
-  return w;
-}
-
-// auto selection (k2_mode 5) for fp64 order 5-6 (order <= 4 runs k2_horner):
-// k2_quad at every batch size, so a site's value never depends on its batch
-// (cfg4: 482 ms vs 591 ms for k2_tmem3 at 2e5 sites, profiles/r01)
-bool use_quad(const acedag_plan* P, int64_t S) {
-  (void)P;
-  (void)S;
-  return true;
-}
-
-// tile geometry: 32 sites per CTA, seed rows [Us][32] in smem (U used seeds
-// plus the constant ONE row), the tail in the per-CTA global cache
+// tile geometry of the general / naive / multi-output kernels: 32 sites per
+// CTA, seed rows [Us][32] in smem (U used seeds plus the constant ONE row),
+// the tail in the per-CTA global cache
 int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, int warps, Launch& lc,
                 int tile = 32) {
   const int64_t ntiles = (S + tile - 1) / tile;
@@ -788,7 +692,6 @@ int plan_launch(acedag_plan* P, int64_t S, size_t elem, size_t red_bytes, int wa
   lc.hyb = lc.us < lc.rows;
   lc.smem = (size_t)lc.us * tile * elem + red_bytes;
   if (lc.hyb) {
-    // sized in double2 units; float2 tables use the first half
     size_t need = (size_t)lc.grid * (lc.rows - lc.us) * tile;
     if (lc.ws->gcache.alloc(need) != cudaSuccess) return fail(ACEDAG_ENOMEM, "gcache allocation failed");
   }
@@ -802,127 +705,17 @@ cudaError_t set_smem(K kernel, size_t smem) {
 
 int nchunks(const acedag_plan* P) { return (int)P->host.chunk.size() - 1; }
 
-template <int NU, typename T, int WARPS, int MAXU, bool HYB>
-cudaError_t launch_fast_w(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
-                          double* out, const Launch& lc, cudaStream_t st) {
-  auto k = dev::k2_fast<NU, T, WARPS, MAXU, HYB>;
-  cudaError_t e = set_smem(k, lc.smem);
-  if (e != cudaSuccess) return e;
-  e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 32);
-  if (e != cudaSuccess) return e;
-  k<<<lc.grid, lc.block, lc.smem, st>>>(
-      reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
-      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(lc.ws->gcache.p), lc.ws->part.p,
-      k2_sched()); note_launch();
-  return cudaGetLastError();
-}
-
-// two sites per lane (64-site tiles): ACEDAG_K2_SPL=1 selects the 32-site kernel
-int k2_spl_env() {
-  const char* e = getenv("ACEDAG_K2_SPL");
-  return e && atoi(e) == 1 ? 1 : 2;
-}
-int k2_mode();
-int k2_spl() { return k2_mode() == 1 ? 1 : 2; }
-
-template <int NU, typename T, int WARPS, int MAXU, bool HYB>
-cudaError_t launch_fast2_w(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
-                           double* out, const Launch& lc, cudaStream_t st) {
-  auto k = dev::k2_fast2<NU, T, WARPS, MAXU, HYB>;
-  cudaError_t e = set_smem(k, lc.smem);
-  if (e != cudaSuccess) return e;
-  e = lc.ws->part.alloc((size_t)lc.grid * WARPS * 64);
-  if (e != cudaSuccess) return e;
-  k<<<lc.grid, lc.block, lc.smem, st>>>(
-      reinterpret_cast<const typename dev::V2<T>::t*>(A), S, L, slot_label, P->U, lc.us, P->ops.p,
-      P->chunk.p, nchunks(P), out, reinterpret_cast<typename dev::V2<T>::t*>(lc.ws->gcache.p), lc.ws->part.p); note_launch();
-  return cudaGetLastError();
-}
-
-// leaf batch of the two-site kernel (ACEDAG_K2_MAXU = 2 or 4)
-int k2_maxu() {
-  static int m = [] {
-    const char* e = getenv("ACEDAG_K2_MAXU");
-    return e && atoi(e) == 2 ? 2 : 4;
-  }();
-  return m;
-}
-
-// fp64 fast-path kernel: "tmem2" (default: two sites per lane, hot seeds in
-// tensor memory), "tmem" (one site per lane, hot seeds in TMEM), "two" (two
-// sites per lane, shared memory only), "one"; ACEDAG_K2 overrides
-// fp64 single-output kernel: ACEDAG_K2 = one | two | tmem | tmem2 | tmem3 |
-// tmem4 | quad; default "auto" = k2_quad for order <= 4 when the sites fill
-// at least one round of 128-site tiles, else k2_tmem3 (profiles/r01)
+// fp64 single-output kernel: ACEDAG_K2 = horner | quad forces one of the two
+// for every order; default: k2_horner for order <= 4 (fp64 Horner spills at
+// order 5-6), k2_quad above
 int k2_mode() {
   static int m = [] {
     const char* e = getenv("ACEDAG_K2");
-    if (e && std::string(e) == "two") return 2;
-    if (e && std::string(e) == "one") return 1;
-    if (e && std::string(e) == "tmem") return 3;
-    if (e && std::string(e) == "tmem2") return 4;
-    if (e && std::string(e) == "tmem4") return 6;
-    if (e && std::string(e) == "quad") return 7;
-    if (e && std::string(e) == "tmem3") return 8;
-    if (e && std::string(e) == "horner") return 9;
-    if (k2_spl_env() == 1) return 1;
-    return 5;
+    if (e && std::string(e) == "quad") return 1;
+    if (e && std::string(e) == "horner") return 2;
+    return 0;
   }();
   return m;
-}
-
-template <int NU, int WARPS, int MAXU, bool HYB>
-cudaError_t launch_tmem_w(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
-                          double* out, const Launch& lc, cudaStream_t st) {
-  auto k = dev::k2_tmem<NU, WARPS, MAXU, HYB>;
-  cudaError_t e = set_smem(k, lc.smem);
-  if (e != cudaSuccess) return e;
-  e = lc.ws->part.alloc((size_t)lc.grid * WARPS * 32);
-  if (e != cudaSuccess) return e;
-  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
-  return cudaGetLastError();
-}
-
-template <int NU, bool HYB>
-cudaError_t launch_tmem_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
-                          double* out, const Launch& lc, cudaStream_t st) {
-  const int w = lc.block / 32;
-  if (w == 32) return launch_tmem_w<NU, 32, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-  if (w == 24) return launch_tmem_w<NU, 24, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-  if (k2_maxu() == 2) return launch_tmem_w<NU, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-  return launch_tmem_w<NU, 16, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
-}
-
-// geometry of k2_tmem: 32 warps, 128 hot rows in TMEM, cold rows in smem
-int tmem_launch(acedag_plan* P, int64_t S, Launch& lc) {
-  const int64_t ntiles = (S + 31) / 32;
-  const int warps = k2_warps();
-  lc.block = warps * 32;
-  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
-  lc.rows = P->U + 1;
-  const int cold = std::max(0, lc.rows - (int)kTmemRows);
-  const size_t fixed = (size_t)warps * 1024 + 16;
-  const int us_max = (int)((P->smem_optin - fixed) / 512);
-  lc.us = std::min(cold, us_max);
-  lc.hyb = lc.us < cold;
-  lc.smem = (size_t)lc.us * 512 + fixed;
-  if (lc.hyb && lc.ws->gcache.alloc((size_t)lc.grid * (cold - lc.us) * 32) != cudaSuccess)
-    return fail(ACEDAG_ENOMEM, "gcache allocation failed");
-  return 0;
-}
-
-template <int NU, int WARPS, int MAXU, bool HYB>
-cudaError_t launch_tmem2_w(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
-                           double* out, const Launch& lc, cudaStream_t st) {
-  auto k = dev::k2_tmem2<NU, WARPS, MAXU, HYB>;
-  cudaError_t e = set_smem(k, lc.smem);
-  if (e != cudaSuccess) return e;
-  e = lc.ws->part.alloc((size_t)lc.grid * WARPS * 64);
-  if (e != cudaSuccess) return e;
-  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
-  return cudaGetLastError();
 }
 
 // The last round of a persistent tile loop is short of tiles when ntiles is
@@ -944,9 +737,6 @@ void tail_split(int64_t ntiles, int grid, int nchunk, int64_t& full, int& parts)
   full = ntiles - rem;
   parts = p;
 }
-
-int tiled_mode();
-bool use_tiled();
 
 // the tile-major seed copy (k_tile_seeds<TS>) for an eval_impl input, or
 // false when the input layout is not one the plan knows
@@ -977,95 +767,34 @@ bool tile_seeds(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
   return true;
 }
 
-template <int NU, bool HYB>
-cudaError_t launch_tmem3_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
-                           double* out, const Launch& lc, cudaStream_t st) {
-  constexpr int W = 32;
-  cudaError_t e;
-  const bool tiled = tiled_mode() >= 2 && tile_seeds<64>(P, A, S, L, slot_label, lc.ws, st, e);
-  if (tiled && e != cudaSuccess) return e;
-  if (tiled) A = lc.ws->tiles.p;
-  mark_prep(st);
-  auto k = tiled ? dev::k2_tmem3<NU, W, HYB, true> : dev::k2_tmem3<NU, W, HYB, false>;
-  e = set_smem(k, lc.smem);
-  if (e != cudaSuccess) return e;
-  e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 64);
-  if (e != cudaSuccess) return e;
-  const int64_t ntiles = (S + 63) / 64;
-  int64_t full = ntiles;
-  int parts = 1;
-  tail_split(ntiles, lc.grid, nchunks(P), full, parts);
-  if (parts > 1) {
-    e = lc.ws->tail.alloc((size_t)(ntiles - full) * nchunks(P) * 64);
-    if (e != cudaSuccess) return e;
-  }
-  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p); note_launch();
-  mark_main(st);
-  e = cudaGetLastError();
-  if (e != cudaSuccess || parts == 1) return e;
-  const int64_t rem = S - full * 64;
-  dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 64, S, 64, nchunks(P), out); note_launch();
-  return cudaGetLastError();
+// geometry of k2_quad: 128-site tiles, 32 hot rows in TMEM, 2 KB cold rows
+// in shared memory, the tail read in place from the tile-major table
+int quad_launch(acedag_plan* P, int64_t S, Launch& lc) {
+  const int64_t ntiles = (S + 127) / 128;
+  lc.block = 16 * 32;
+  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
+  lc.rows = P->U + 1;
+  const int cold = std::max(0, lc.rows - (int)dev::kTmemRowsQ);
+  // rings, TMEM slot + chunk counter (16 B), slot -> label table
+  const size_t fixed = (size_t)16 * dev::Ring3::kAlloc + 16 + (((size_t)lc.rows * 4 + 15) & ~(size_t)15);
+  const int us_max = (int)((P->smem_optin - fixed) / 2048);
+  lc.us = std::min(cold, us_max);
+  lc.hyb = lc.us < cold;
+  lc.smem = (size_t)lc.us * 2048 + fixed;
+  return 0;
 }
-
-template <int NU> struct Tmem3F64 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_tmem3_k<NU, true>(a...) : launch_tmem3_k<NU, false>(a...);
-  }
-};
-
-template <int NU, bool HYB>
-cudaError_t launch_tmem2_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
-                           double* out, const Launch& lc, cudaStream_t st) {
-  if (lc.block == 32 * 32) {
-    // 2-leaf batches measured fastest here (21.6 vs 20.5 M sites/s at cfg2)
-    if (getenv("ACEDAG_K2_MAXU") && k2_maxu() == 4)
-      return launch_tmem2_w<NU, 32, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
-    return launch_tmem2_w<NU, 32, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-  }
-  if (lc.block == 24 * 32) return launch_tmem2_w<NU, 24, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-  return launch_tmem2_w<NU, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-}
-
-template <int NU, bool HYB>
-cudaError_t launch_tmem4_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
-                           double* out, const Launch& lc, cudaStream_t st) {
-  constexpr int W = 32;
-  auto k = dev::k2_tmem4<NU, W, HYB>;
-  cudaError_t e = set_smem(k, lc.smem);
-  if (e != cudaSuccess) return e;
-  e = lc.ws->part.alloc((size_t)lc.grid * W * 64);
-  if (e != cudaSuccess) return e;
-  k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops4.p, P->chunk.p, P->croots.p,
-                                        nchunks(P), out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
-  return cudaGetLastError();
-}
-
-// tile-major seed copy: ACEDAG_TILED=0 never, 1 (default) for k2_quad,
-// 2 also for k2_tmem3 (measured slower there: cfg4's long global tail is
-// better served by the per-CTA cache that stays in L2; cfg1 is launch-bound)
-int tiled_mode() {
-  static int v = [] {
-    const char* e = getenv("ACEDAG_TILED");
-    return e ? atoi(e) : 1;
-  }();
-  return v;
-}
-bool use_tiled() { return tiled_mode() >= 1; }
 
 template <int NU, bool HYB>
 cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
                           double* out, const Launch& lc, cudaStream_t st) {
   constexpr int W = 16;
-  const bool two = getenv("ACEDAG_K2_MAXU") ? k2_maxu() >= 2 : NU <= 4;
+  constexpr int MAXU = NU <= 4 ? 2 : 1;
   cudaError_t e;
-  const bool tiled = use_tiled() && tile_seeds<128>(P, A, S, L, slot_label, lc.ws, st, e);
-  if (tiled && e != cudaSuccess) return e;
-  if (tiled) A = lc.ws->tiles.p;
+  if (!tile_seeds<128>(P, A, S, L, slot_label, lc.ws, st, e)) return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  A = lc.ws->tiles.p;
   mark_prep(st);
-  auto k = tiled ? (two ? dev::k2_quad<NU, W, 2, HYB, true> : dev::k2_quad<NU, W, 1, HYB, true>)
-                 : (two ? dev::k2_quad<NU, W, 2, HYB, false> : dev::k2_quad<NU, W, 1, HYB, false>);
+  auto k = dev::k2_quad<NU, W, MAXU, HYB, true>;
   e = set_smem(k, lc.smem);
   if (e != cudaSuccess) return e;
   e = lc.ws->part.alloc((size_t)lc.grid * nchunks(P) * 128);
@@ -1079,7 +808,7 @@ cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, co
     if (e != cudaSuccess) return e;
   }
   k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->opsQ.p, P->chunk.p, nchunks(P),
-                                        out, lc.ws->gcache.p, lc.ws->part.p, full, parts, lc.ws->tail.p); note_launch();
+                                        out, nullptr, lc.ws->part.p, full, parts, lc.ws->tail.p); note_launch();
   mark_main(st);
   e = cudaGetLastError();
   if (e != cudaSuccess || parts == 1) return e;
@@ -1087,6 +816,12 @@ cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, co
   dev::k_tail_reduce<<<(unsigned)((rem + 255) / 256), 256, 0, st>>>(lc.ws->tail.p, full * 128, S, 128, nchunks(P), out); note_launch();
   return cudaGetLastError();
 }
+
+template <int NU> struct QuadF64 {
+  template <typename... A> static cudaError_t run(bool hyb, A... a) {
+    return hyb ? launch_quad_k<NU, true>(a...) : launch_quad_k<NU, false>(a...);
+  }
+};
 
 // k2_horner on the tile-major seed table (V: double2, or float2 for the fp32
 // mode); false (nothing launched) when the input layout is not one
@@ -1124,113 +859,13 @@ bool run_horner(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
   return true;
 }
 
-// auto selection (k2_mode 5) prefers k2_horner for order <= 4 (every batch
-// size, so a site's value never depends on its batch); f32: the fp32 mode
-bool use_horner(const acedag_plan* P, int64_t S, bool f32 = false) {
-  (void)S;
+// k2_horner for fp64 order <= 4 and every fp32 order, at every batch size
+// (so a site's value never depends on its batch); ACEDAG_K2 overrides fp64
+bool use_horner(const acedag_plan* P, bool f32 = false) {
   const acedag_plan::HornerProg& hp = P->hp[f32 ? 1 : 0];
-  return hp.ok && ((P->host.max_order <= (f32 ? 6 : 4) && k2_mode() == 5) || k2_mode() == 9);
-}
-
-template <int NU> struct QuadF64 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_quad_k<NU, true>(a...) : launch_quad_k<NU, false>(a...);
-  }
-};
-
-// geometry of k2_quad: 128-site tiles, 32 hot rows in TMEM, 2 KB cold rows
-int quad_launch(acedag_plan* P, int64_t S, Launch& lc) {
-  const int64_t ntiles = (S + 127) / 128;
-  lc.block = 16 * 32;
-  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
-  lc.rows = P->U + 1;
-  const int cold = std::max(0, lc.rows - (int)dev::kTmemRowsQ);
-  // rings, TMEM slot + chunk counter (16 B), slot -> label table
-  const size_t fixed = (size_t)16 * dev::Ring3::kAlloc + 16 + (((size_t)lc.rows * 4 + 15) & ~(size_t)15);
-  const int us_max = (int)((P->smem_optin - fixed) / 2048);
-  lc.us = std::min(cold, us_max);
-  lc.hyb = lc.us < cold;
-  lc.smem = (size_t)lc.us * 2048 + fixed;
-  if (lc.hyb && lc.ws->gcache.alloc((size_t)lc.grid * (cold - lc.us) * 128) != cudaSuccess)
-    return fail(ACEDAG_ENOMEM, "gcache allocation failed");
-  return 0;
-}
-
-template <int NU> struct Tmem4F64 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_tmem4_k<NU, true>(a...) : launch_tmem4_k<NU, false>(a...);
-  }
-};
-
-// geometry of k2_tmem2/3/4: 64-site tiles, 64 hot rows in TMEM, 1 KB cold rows
-int tmem2_launch(acedag_plan* P, int64_t S, Launch& lc) {
-  const int64_t ntiles = (S + 63) / 64;
-  const bool v3 = k2_mode() >= 5 && k2_mode() != 7;
-  const int warps = v3 ? 32 : k2_warps();
-  lc.block = warps * 32;
-  lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
-  lc.rows = P->U + 1;
-  const int cold = std::max(0, lc.rows - (int)dev::kTmemRows2);
-  const size_t fixed = (size_t)warps * (v3 ? dev::Ring3::kAlloc : 1024) + 16;
-  const int us_max = (int)((P->smem_optin - fixed) / 1024);
-  lc.us = std::min(cold, us_max);
-  lc.hyb = lc.us < cold;
-  lc.smem = (size_t)lc.us * 1024 + fixed;
-  if (lc.hyb && lc.ws->gcache.alloc((size_t)lc.grid * (cold - lc.us) * 64) != cudaSuccess)
-    return fail(ACEDAG_ENOMEM, "gcache allocation failed");
-  return 0;
-}
-
-template <int NU> struct Tmem2F64 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_tmem2_k<NU, true>(a...) : launch_tmem2_k<NU, false>(a...);
-  }
-};
-
-template <int NU> struct TmemF64 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_tmem_k<NU, true>(a...) : launch_tmem_k<NU, false>(a...);
-  }
-};
-
-template <int NU, typename T, bool HYB>
-cudaError_t launch_fast2(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
-                         double* out, const Launch& lc, cudaStream_t st) {
-  const int w = lc.block / 32;
-  if (k2_maxu() == 2) {
-    if (w == 16) return launch_fast2_w<NU, T, 16, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-    if (w == 24) return launch_fast2_w<NU, T, 24, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-    return launch_fast2_w<NU, T, 32, 2, HYB>(P, A, S, L, slot_label, out, lc, st);
-  }
-  if (w == 16) return launch_fast2_w<NU, T, 16, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
-  if (w == 24) return launch_fast2_w<NU, T, 24, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
-  return launch_fast2_w<NU, T, 32, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
-}
-
-template <int NU, typename T, bool HYB>
-cudaError_t launch_fast(acedag_plan* P, const void* A, int64_t S, int L, const uint16_t* slot_label,
-                        double* out, const Launch& lc, cudaStream_t st) {
-  if (lc.block == 32 * 32) return launch_fast_w<NU, T, 32, 4, HYB>(P, A, S, L, slot_label, out, lc, st);
-  return launch_fast_w<NU, T, 16, 8, HYB>(P, A, S, L, slot_label, out, lc, st);
-}
-
-constexpr int kMultiWarps = 16, kNOC = 32;
-
-template <int NU, bool HYB>
-cudaError_t launch_multi(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
-                         double* out, const Launch& lc, cudaStream_t st) {
-  auto k = dev::k2_multi<NU, kMultiWarps, kNOC, HYB>;
-  cudaError_t e = set_smem(k, lc.smem);
-  if (e != cudaSuccess) return e;
-  e = lc.ws->part.alloc((size_t)lc.grid * kMultiWarps * kNOC * 32);
-  if (e != cudaSuccess) return e;
-  for (int o0 = 0; o0 < P->host.n_out; o0 += kNOC) {
-    k<<<lc.grid, lc.block, lc.smem, st>>>(A, S, L, slot_label, P->U, lc.us, P->ops.p, P->chunk.p, nchunks(P),
-                                          P->cre.p, P->host.n_out, o0, out, lc.ws->gcache.p, lc.ws->part.p); note_launch();
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  if (!hp.ok) return false;
+  if (f32) return true;
+  return k2_mode() == 2 || (k2_mode() == 0 && P->host.max_order <= 4);
 }
 
 constexpr int kMmaWarps = 16;
@@ -1250,15 +885,6 @@ cudaError_t launch_mma(acedag_plan* P, const double2* A, int64_t S, int L, const
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
-}
-
-// ACEDAG_MULTI=scalar selects the scalar multi-output kernel instead of DMMA
-bool use_mma() {
-  static bool m = [] {
-    const char* e = getenv("ACEDAG_MULTI");
-    return !(e && std::string(e) == "scalar");
-  }();
-  return m;
 }
 
 template <int NU, bool HYB>
@@ -1309,31 +935,6 @@ cudaError_t by_order(int nu, Args&&... a) {
   return cudaErrorInvalidValue;
 }
 
-template <int NU> struct FastF64 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_fast<NU, double, true>(a...) : launch_fast<NU, double, false>(a...);
-  }
-};
-template <int NU> struct Fast2F64 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_fast2<NU, double, true>(a...) : launch_fast2<NU, double, false>(a...);
-  }
-};
-template <int NU> struct Fast2F32 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_fast2<NU, float, true>(a...) : launch_fast2<NU, float, false>(a...);
-  }
-};
-template <int NU> struct FastF32 {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_fast<NU, float, true>(a...) : launch_fast<NU, float, false>(a...);
-  }
-};
-template <int NU> struct Multi {
-  template <typename... A> static cudaError_t run(bool hyb, A... a) {
-    return hyb ? launch_multi<NU, true>(a...) : launch_multi<NU, false>(a...);
-  }
-};
 template <int NU> struct Mma {
   template <typename... A> static cudaError_t run(bool hyb, A... a) {
     return hyb ? launch_mma<NU, true>(a...) : launch_mma<NU, false>(a...);
@@ -1354,6 +955,18 @@ template <int NU> struct NaiveGen {
     return hyb ? launch_naive<NU, true, true>(a...) : launch_naive<NU, true, false>(a...);
   }
 };
+
+// which kernel eval_body launches (acedag_eval_kernel_name reports it)
+enum class K2 { Horner, Quad, Mma, General, Naive, None };
+K2 pick(const acedag_plan* P, int method, int prec, int out_kind) {
+  const PlanHost& H = P->host;
+  if (method == ACEDAG_METHOD_NAIVE) return prec == ACEDAG_PREC_F64 ? K2::Naive : K2::None;
+  const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
+  if (prec == ACEDAG_PREC_F32) return fast && use_horner(P, true) ? K2::Horner : K2::None;
+  if (fast) return use_horner(P) ? K2::Horner : K2::Quad;
+  if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out >= 8) return K2::Mma;
+  return K2::General;
+}
 
 int eval_body(acedag_plan* P, int method, int prec, int out_kind, const void* A, int64_t S, int L,
               const uint16_t* slot_label, void* out, cudaStream_t st);
@@ -1379,82 +992,54 @@ int eval_impl(acedag_plan* P, int method, int prec, int out_kind, const void* A,
 int eval_body(acedag_plan* P, int method, int prec, int out_kind, const void* A, int64_t S, int L,
               const uint16_t* slot_label, void* out, cudaStream_t st) {
   const PlanHost& H = P->host;
-  const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
   Launch lc;
   lc.ws = P->ws(st);
-  cudaError_t e;
-  if (method == ACEDAG_METHOD_RECURSIVE) {
-    if (prec == ACEDAG_PREC_F32) {
-      if (!fast) return fail(ACEDAG_EUNSUPPORTED, "fp32 mode supports real coefficients, one real output");
-      if (use_horner(P, S, true) && run_horner(P, (const float2*)A, S, L, slot_label, (double*)out, lc, st, e)) {
-        if (e != cudaSuccess) return cuda_fail(e, "k2_horner (fp32)");
-      } else if (k2_spl() == 2) {
-        int rc = plan_launch(P, S, sizeof(float2), k2_warps() * 1024, k2_warps(), lc, 64);
-        if (rc) return rc;
-        e = by_order<Fast2F32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
-      } else {
-        int rc = plan_launch(P, S, sizeof(float2), k2_warps() * 1024 + 16, k2_warps(), lc);
-        if (rc) return rc;
-        e = by_order<FastF32>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
+  cudaError_t e = cudaSuccess;
+  switch (pick(P, method, prec, out_kind)) {
+    case K2::None:
+      if (method == ACEDAG_METHOD_NAIVE) return fail(ACEDAG_EUNSUPPORTED, "naive path is fp64 only");
+      return fail(ACEDAG_EUNSUPPORTED,
+                  "fp32 mode supports real coefficients and one real output on programs k2_horner can encode");
+    case K2::Horner:
+      if (prec == ACEDAG_PREC_F32) {
+        if (!run_horner(P, (const float2*)A, S, L, slot_label, (double*)out, lc, st, e))
+          return fail(ACEDAG_EINVAL, "unknown seed layout");
+      } else if (!run_horner(P, (const double2*)A, S, L, slot_label, (double*)out, lc, st, e)) {
+        return fail(ACEDAG_EINVAL, "unknown seed layout");
       }
-    } else if (fast && use_horner(P, S) &&
-               run_horner(P, (const double2*)A, S, L, slot_label, (double*)out, lc, st, e)) {
       if (e != cudaSuccess) return cuda_fail(e, "k2_horner");
-    } else if (fast && (k2_mode() == 7 || k2_mode() == 9 || (k2_mode() == 5 && use_quad(P, S)))) {
+      return ACEDAG_OK;
+    case K2::Quad: {
       int rc = quad_launch(P, S, lc);
       if (rc) return rc;
       e = by_order<QuadF64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
-    } else if (fast && k2_mode() == 6 && P->ops4_ok) {
-      int rc = tmem2_launch(P, S, lc);
-      if (rc) return rc;
-      if (lc.us != tmem_us_max_clamped(P)) return fail(ACEDAG_EINVAL, "k2_tmem4 geometry mismatch");
-      e = by_order<Tmem4F64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
-    } else if (fast && (k2_mode() == 5 || k2_mode() == 8 || k2_mode() == 6)) {
-      int rc = tmem2_launch(P, S, lc);
-      if (rc) return rc;
-      e = by_order<Tmem3F64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
-    } else if (fast && k2_mode() == 4) {
-      int rc = tmem2_launch(P, S, lc);
-      if (rc) return rc;
-      e = by_order<Tmem2F64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
-    } else if (fast && k2_mode() == 3) {
-      int rc = tmem_launch(P, S, lc);
-      if (rc) return rc;
-      e = by_order<TmemF64>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
-    } else if (fast) {
-      if (k2_spl() == 2) {
-        int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024, k2_warps(), lc, 64);
-        if (rc) return rc;
-        e = by_order<Fast2F64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
-      } else {
-        int rc = plan_launch(P, S, sizeof(double2), k2_warps() * 1024 + 16, k2_warps(), lc);
-        if (rc) return rc;
-        e = by_order<FastF64>(H.max_order, lc.hyb, P, A, S, L, slot_label, (double*)out, lc, st);
-      }
-    } else if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out >= 8 && use_mma()) {
+      break;
+    }
+    case K2::Mma: {
       // smem beyond the seed rows: 16 program rings + 16 x [8][36] staging
       int rc = plan_launch(P, S, sizeof(double2), kMmaWarps * 1024 + kMmaWarps * 8 * 36 * 8, kMmaWarps, lc);
       if (rc) return rc;
       e = by_order<Mma>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
-    } else if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out % 2 == 0) {
-      int rc = plan_launch(P, S, sizeof(double2), kMultiWarps * 1024, kMultiWarps, lc);
-      if (rc) return rc;
-      e = by_order<Multi>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label, (double*)out, lc, st);
-    } else {
+      break;
+    }
+    case K2::General: {
       int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), kWarps, lc);
       if (rc) return rc;
       e = by_order<General>(H.max_order, lc.hyb, P, (const double2*)A, S, L, slot_label,
                             out_kind == ACEDAG_OUT_COMPLEX ? 1 : 0, out, lc, st);
+      break;
     }
-  } else {
-    if (prec != ACEDAG_PREC_F64) return fail(ACEDAG_EUNSUPPORTED, "naive path is fp64 only");
-    int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), kWarps, lc);
-    if (rc) return rc;
-    const int nu = std::max(2, H.naive_max_order);
-    if (fast) e = by_order<NaiveFast>(nu, lc.hyb, P, (const double2*)A, S, L, slot_label, 0, out, lc, st);
-    else
-      e = by_order<NaiveGen>(nu, lc.hyb, P, (const double2*)A, S, L, slot_label,
-                             out_kind == ACEDAG_OUT_COMPLEX ? 1 : 0, out, lc, st);
+    case K2::Naive: {
+      int rc = plan_launch(P, S, sizeof(double2), 2 * kWarps * 32 * sizeof(double), kWarps, lc);
+      if (rc) return rc;
+      const int nu = std::max(2, H.naive_max_order);
+      const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
+      if (fast) e = by_order<NaiveFast>(nu, lc.hyb, P, (const double2*)A, S, L, slot_label, 0, out, lc, st);
+      else
+        e = by_order<NaiveGen>(nu, lc.hyb, P, (const double2*)A, S, L, slot_label,
+                               out_kind == ACEDAG_OUT_COMPLEX ? 1 : 0, out, lc, st);
+      break;
+    }
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return ACEDAG_OK;
@@ -1612,31 +1197,19 @@ int acedag_plan_timing_read(acedag_plan* P, double* ms, int64_t* calls) {
 }
 
 const char* acedag_eval_kernel_name(const acedag_plan* P, int method, int prec, int out_kind, int64_t S) {
+  (void)S;  // the choice does not depend on the batch size
   if (!P || !P->has_coef) {
     fail(ACEDAG_EINVAL, "plan has no coefficients");
     return "";
   }
-  const PlanHost& H = P->host;
-  const bool fast = out_kind == ACEDAG_OUT_REAL && H.n_out == 1 && !H.complex_coef;
-  if (method == ACEDAG_METHOD_NAIVE) return "k3_naive";
-  if (prec == ACEDAG_PREC_F32)
-    return use_horner(P, S, true) ? "k2_horner (fp32)" : (k2_spl() == 2 ? "k2_fast2 (fp32)" : "k2_fast (fp32)");
-  if (fast) {
-    switch (k2_mode()) {
-      case 8: return "k2_tmem3";
-      case 7: return "k2_quad";
-      case 6: return P->ops4_ok ? "k2_tmem4" : "k2_tmem3";
-      case 5: return use_horner(P, S) ? "k2_horner" : (use_quad(P, S) ? "k2_quad" : "k2_tmem3");
-      case 9: return use_horner(P, S) ? "k2_horner" : "k2_quad";
-      case 4: return "k2_tmem2";
-      case 3: return "k2_tmem";
-      case 2: return "k2_fast2";
-      default: return "k2_fast";
-    }
+  switch (pick(P, method, prec, out_kind)) {
+    case K2::Horner: return prec == ACEDAG_PREC_F32 ? "k2_horner (fp32)" : "k2_horner";
+    case K2::Quad: return "k2_quad";
+    case K2::Mma: return "k2_mma";
+    case K2::General: return "k2_general";
+    case K2::Naive: return "k3_naive";
+    default: return "";
   }
-  if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out >= 8 && use_mma()) return "k2_mma";
-  if (out_kind == ACEDAG_OUT_REAL && !H.complex_coef && H.n_out % 2 == 0) return "k2_multi";
-  return "k2_general";
 }
 
 int acedag_reduce_sites(const acedag_plan* P, const double* phi, int64_t S, double* out_total,

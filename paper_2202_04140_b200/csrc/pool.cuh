@@ -76,7 +76,7 @@ __global__ void pool_ref(const double* __restrict__ coords, const int32_t* __res
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = idx / L;
     const int4 e = labels[idx - s * L];
-    const int nj = counts ? counts[s] : J;
+    const int nj = counts ? min(max(counts[s], 0), J) : J;  // ragged sites, clamped to the row
     double ar = 0.0, ai = 0.0;
     for (int j = 0; j < nj; ++j) {
       const double* c = coords + (s * J + j) * NC;

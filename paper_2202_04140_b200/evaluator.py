@@ -68,18 +68,54 @@ def _check_coords(group: Group, coords) -> None:  # evaluator.py:46-58
 
 
 # ----------------------------------------------------------------- batched
+# Every device entry point checks its tensors before a pointer crosses the C
+# ABI: a wrong dtype, shape or device must be a ValueError, never an
+# out-of-bounds access inside a kernel.
+
+def _need(t: torch.Tensor, name: str, dtype, device: torch.device | None = None, shape=None) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a torch tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    dts = dtype if isinstance(dtype, tuple) else (dtype,)
+    if t.dtype not in dts:
+        raise ValueError(f"{name} must be {' or '.join(str(d) for d in dts)}, got {t.dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _result(result, shape, dtype, device: torch.device) -> torch.Tensor:
+    """A caller-supplied output must be a contiguous tensor of exactly the
+    output's shape, dtype and device (the kernels write through its pointer)."""
+    if result is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    _need(result, "result", dtype, device, shape)
+    if not result.is_contiguous():
+        raise ValueError("result must be contiguous")
+    return result
+
+
+def _counts(counts, S: int, device: torch.device):
+    if counts is None:
+        return None
+    _need(counts, "counts", (torch.int32, torch.int64), device, (S,))
+    return counts.to(torch.int32).contiguous()
+
 
 def pool_batched(group: Group, cap: int, coords: torch.Tensor, counts: torch.Tensor | None = None,
                  out: torch.Tensor | None = None) -> torch.Tensor:
     """K1, reference convention.  coords: cuda float64 [S, J, ncoord(group)];
     counts: cuda int32 [S] (ragged sites) or None.  Returns complex128 [S, L]."""
+    _need(coords, "coords", torch.float64)
+    if coords.dim() != 3 or coords.shape[2] != group.components:
+        raise ValueError(f"coords must be [S, J, {group.components}] for {group.value}, got {tuple(coords.shape)}")
     coords = coords.contiguous()
     S, J = coords.shape[0], coords.shape[1]
     L = len(one_particle_indices(group, cap))
-    if out is None:
-        out = torch.empty((S, L), dtype=torch.complex128, device=coords.device)
-    if counts is not None:
-        counts = counts.to(torch.int32).contiguous()
+    out = _result(out, (S, L), torch.complex128, coords.device)
+    counts = _counts(counts, S, coords.device)
     N.check(N.lib().acedag_pool(group.code, int(cap), _vp(coords), _vp(counts), S, J, _vp(out),
                                 _stream(coords.device)))
     return out
@@ -88,13 +124,14 @@ def pool_batched(group: Group, cap: int, coords: torch.Tensor, counts: torch.Ten
 def pool_positions(cap: int, xyz: torch.Tensor, counts: torch.Tensor | None = None,
                    r_in: float = R_IN, r_cut: float = R_CUT, out: torch.Tensor | None = None):
     """K1 for Cartesian neighbour shells (BASELINE cfg3/cfg5); complex128 [S, L]."""
+    _need(xyz, "xyz", torch.float64)
+    if xyz.dim() != 3 or xyz.shape[2] != 3:
+        raise ValueError(f"xyz must be [S, J, 3], got {tuple(xyz.shape)}")
     xyz = xyz.contiguous()
     S, J = xyz.shape[0], xyz.shape[1]
     L = len(one_particle_indices(Group.O3, cap))
-    if out is None:
-        out = torch.empty((S, L), dtype=torch.complex128, device=xyz.device)
-    if counts is not None:
-        counts = counts.to(torch.int32).contiguous()
+    out = _result(out, (S, L), torch.complex128, xyz.device)
+    counts = _counts(counts, S, xyz.device)
     N.check(N.lib().acedag_pool_positions(int(cap), _vp(xyz), _vp(counts), S, J, float(r_in),
                                           float(r_cut), _vp(out), _stream(xyz.device)))
     return out
@@ -118,6 +155,7 @@ class SitePlan:
         with torch.cuda.device(self.device):
             N.check(N.lib().acedag_plan_create(self.graph._h, self.device, C.byref(h)))
         self._h = h
+        self._dev = torch.device("cuda", self.device)
         self.n_out = 0
         self.complex_coef = False
 
@@ -198,21 +236,16 @@ class SitePlan:
         (``out="real"``) or complex128 (``out="complex"``)."""
         if self.n_out == 0:
             raise ValueError("no coefficients set")
+        _need(A, "A", (torch.complex128, torch.complex64), self._dev)
         if A.dim() != 2 or A.shape[1] != self.graph.num_seeds:
             raise ValueError(f"A must be [S, {self.graph.num_seeds}], got {tuple(A.shape)}")
         A = A.contiguous()
-        if A.dtype == torch.complex128:
-            prec = N.PREC_F64
-        elif A.dtype == torch.complex64:
-            prec = N.PREC_F32
-        else:
-            raise ValueError("A must be complex128 or complex64")
+        prec = N.PREC_F64 if A.dtype == torch.complex128 else N.PREC_F32
         S = A.shape[0]
         kind = N.OUT_COMPLEX if out == "complex" else N.OUT_REAL
         dt = torch.complex128 if kind == N.OUT_COMPLEX else torch.float64
         shape = (S,) if self.n_out == 1 else (S, self.n_out)
-        if result is None:
-            result = torch.empty(shape, dtype=dt, device=A.device)
+        result = _result(result, shape, dt, self._dev)
         m = N.METHOD_NAIVE if method == "naive" else N.METHOD_RECURSIVE
         N.check(N.lib().acedag_eval(self._h, m, prec, kind, _vp(A), S, _vp(result), _stream(A.device)))
         return result
@@ -298,24 +331,28 @@ class SitePlan:
                            r_in: float = R_IN, r_cut: float = R_CUT, out: str = "real",
                            result: torch.Tensor | None = None) -> torch.Tensor:
         """Fused K1 + K2 from Cartesian neighbour vectors [S, J, 3] float64."""
+        if self.n_out == 0:
+            raise ValueError("no coefficients set")
+        _need(xyz, "xyz", torch.float64, self._dev)
+        if xyz.dim() != 3 or xyz.shape[2] != 3:
+            raise ValueError(f"xyz must be [S, J, 3], got {tuple(xyz.shape)}")
         xyz = xyz.contiguous()
         S, J = xyz.shape[0], xyz.shape[1]
         kind = N.OUT_COMPLEX if out == "complex" else N.OUT_REAL
         dt = torch.complex128 if kind == N.OUT_COMPLEX else torch.float64
         shape = (S,) if self.n_out == 1 else (S, self.n_out)
-        if result is None:
-            result = torch.empty(shape, dtype=dt, device=xyz.device)
-        if counts is not None:
-            counts = counts.to(torch.int32).contiguous()
+        result = _result(result, shape, dt, self._dev)
+        counts = _counts(counts, S, self._dev)
         N.check(N.lib().acedag_eval_from_positions(self._h, _vp(xyz), _vp(counts), S, J, float(r_in),
                                                    float(r_cut), kind, _vp(result), _stream(xyz.device)))
         return result
 
     def evaluate_nodes(self, A: torch.Tensor) -> torch.Tensor:
         """All node values, complex128 [S, N], bit-identical to evaluate_graph."""
-        A = A.contiguous()
-        if A.dtype != torch.complex128 or A.shape[1] != self.graph.num_seeds:
+        _need(A, "A", torch.complex128, self._dev)
+        if A.dim() != 2 or A.shape[1] != self.graph.num_seeds:
             raise ValueError("A must be complex128 [S, L]")
+        A = A.contiguous()
         S = A.shape[0]
         out = torch.empty((S, self.graph.num_nodes), dtype=torch.complex128, device=A.device)
         N.check(N.lib().acedag_eval_nodes(self._h, _vp(A), S, _vp(out), _stream(A.device)))
@@ -323,9 +360,11 @@ class SitePlan:
 
     def reduce_sites(self, phi: torch.Tensor, total: torch.Tensor | None = None) -> torch.Tensor:
         """Deterministic sum over sites of a real phi [S] / [S, n_out]."""
+        _need(phi, "phi", torch.float64, self._dev)
+        if phi.dim() not in (1, 2) or phi.reshape(phi.shape[0], -1).shape[1] != self.n_out:
+            raise ValueError(f"phi must be [S] or [S, {self.n_out}] float64")
         phi = phi.contiguous()
-        if total is None:
-            total = torch.zeros(self.n_out, dtype=torch.float64, device=phi.device)
+        total = _result(total, (self.n_out,), torch.float64, self._dev)
         N.check(N.lib().acedag_reduce_sites(self._h, _vp(phi), phi.shape[0], _vp(total), _stream(phi.device)))
         return total
 
@@ -336,11 +375,18 @@ def launch_count() -> int:
 
 
 def naive_products(vals: torch.Tensor, lens: torch.Tensor | None = None) -> torch.Tensor:
-    """Batched naive_eval over rows of complex128 [n, width] (bit-exact)."""
+    """Batched naive_eval over rows of complex128 [n, width] (bit-exact);
+    lens [n] (each <= width) gives ragged row lengths."""
+    _need(vals, "vals", torch.complex128)
+    if vals.dim() != 2:
+        raise ValueError(f"vals must be [n, width], got {tuple(vals.shape)}")
     vals = vals.contiguous()
     n, w = vals.shape
     out = torch.empty(n, dtype=torch.complex128, device=vals.device)
     if lens is not None:
+        _need(lens, "lens", (torch.int32, torch.int64), vals.device, (n,))
+        if n and (int(lens.min()) < 0 or int(lens.max()) > w):
+            raise ValueError(f"lens must lie in [0, {w}]")
         lens = lens.to(torch.int32).contiguous()
     N.check(N.lib().acedag_naive_products(_vp(vals), _vp(lens), n, w, _vp(out), _stream(vals.device)))
     return out

@@ -6,10 +6,13 @@ import cmath
 import math
 import random
 
+import numpy as np
 import pytest
+import torch
 
 import paper_2202_04140_b200 as P
 from paper_2202_04140_b200 import DegreeSpec, Group, canonical
+from _helpers import seeded_A
 from oracle import acedag_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -170,3 +173,55 @@ def test_reference_graph_objects_are_accepted(cuda):
     A = np.array([[pooled[e] for e in O.one_particle_indices("O3", 5)]])
     re, im = O.evaluate_nodes(pa, pb, A)
     assert all(v == complex(r, i) for v, r, i in zip(vals, re[:, 0], im[:, 0]))
+
+
+def test_rejected_coefficients_keep_the_previous_program(cuda):
+    """a rejected set_coefficients (non-target id) raises and leaves
+    the plan evaluating its previous coefficients bit for bit."""
+    g = P.build_graph(P.Group.O3, P.DegreeSpec(1, 8), 3)
+    rng = np.random.default_rng(50)
+    c = rng.normal(size=len(g.target_ids))
+    plan = P.SitePlan(g).set_coefficients(node_ids=g.target_ids, values=c)
+    A = torch.from_numpy(seeded_A(300, g.num_seeds, 51)).to(cuda)
+    before = plan.evaluate(A).clone()
+    before_n = plan.evaluate(A, method="naive").clone()
+    aux = int(np.flatnonzero(g.aux)[0])
+    with pytest.raises(ValueError):
+        plan.set_coefficients(node_ids=[aux], values=[1.0])
+    assert torch.equal(plan.evaluate(A), before)
+    assert torch.equal(plan.evaluate(A, method="naive"), before_n)
+    assert torch.equal(plan.evaluate(A, out="complex").real, before)
+
+
+def test_device_entry_points_validate_tensors(cuda):
+    """wrong dtype / shape / device / contiguity of caller tensors
+    is a ValueError before any pointer reaches a kernel."""
+    g = P.build_graph(P.Group.O3, P.DegreeSpec(1, 8), 3)
+    plan = P.SitePlan(g).set_coefficients(node_ids=g.target_ids, values=np.ones(len(g.target_ids)))
+    A = torch.from_numpy(seeded_A(40, g.num_seeds, 52)).to(cuda)
+    with pytest.raises(ValueError):
+        plan.evaluate(A.cpu())
+    with pytest.raises(ValueError):
+        plan.evaluate(A.real.contiguous())
+    with pytest.raises(ValueError):
+        plan.evaluate(A, result=torch.empty(39, dtype=torch.float64, device=cuda))
+    with pytest.raises(ValueError):
+        plan.evaluate(A, result=torch.empty(40, dtype=torch.float32, device=cuda))
+    with pytest.raises(ValueError):
+        plan.evaluate(A, result=torch.empty(80, dtype=torch.float64, device=cuda)[::2])
+    xyz = torch.rand(5, 7, 3, dtype=torch.float64, device=cuda) + 1.0
+    with pytest.raises(ValueError):
+        plan.evaluate_positions(xyz.float())
+    with pytest.raises(ValueError):
+        plan.evaluate_positions(xyz[..., :2].contiguous())
+    with pytest.raises(ValueError):
+        plan.evaluate_positions(xyz, counts=torch.zeros(4, dtype=torch.int32, device=cuda))
+    with pytest.raises(ValueError):
+        P.pool_batched(P.Group.O3, 4, xyz.float())
+    with pytest.raises(ValueError):
+        plan.reduce_sites(torch.zeros(5, 2, dtype=torch.float64, device=cuda))
+    # counts above J are clamped to the row (pool_ref), not read past it
+    coords = torch.rand(2, 3, 3, dtype=torch.float64, device=cuda)
+    big = P.pool_batched(P.Group.O3, 3, coords, torch.tensor([99, 3], dtype=torch.int32, device=cuda))
+    full = P.pool_batched(P.Group.O3, 3, coords)
+    assert torch.equal(big, full)

@@ -190,7 +190,9 @@ def test_rejected_coefficients_keep_the_previous_program(cuda):
         plan.set_coefficients(node_ids=[aux], values=[1.0])
     assert torch.equal(plan.evaluate(A), before)
     assert torch.equal(plan.evaluate(A, method="naive"), before_n)
-    assert torch.equal(plan.evaluate(A, out="complex").real, before)
+    # the complex-output kernel (k2_general) sums in another order: same
+    # coefficients, equal to rounding
+    assert torch.allclose(plan.evaluate(A, out="complex").real, before, rtol=1e-10, atol=1e-9)
 
 
 def test_device_entry_points_validate_tensors(cuda):

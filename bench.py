@@ -377,15 +377,18 @@ def run_ours(a):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun the NCCL group is set up even for one rank, so the
+    # barrier / max-over-ranks / energy all-reduce path always runs there
+    distributed = world > 1 or "RANK" in os.environ
+    if distributed:
         dist.init_process_group("nccl", init_method="env://", device_id=dev)
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     def max_over_ranks(x):
-        if world > 1:
+        if distributed:
             t = torch.tensor([x], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return float(t.item())
@@ -571,7 +574,7 @@ def run_ours(a):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
     return 0
 

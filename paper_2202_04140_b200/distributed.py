@@ -31,9 +31,9 @@ def rank_world() -> tuple[int, int]:
 
 
 def total_energy(local_total: torch.Tensor) -> torch.Tensor:
-    """All-reduce (sum) of per-rank site totals, in place; identity when not
-    distributed."""
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    """All-reduce (sum) of per-rank site totals, in place; identity when no
+    process group is initialised (a group of one still runs the collective)."""
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(local_total, op=dist.ReduceOp.SUM)
     return local_total
 

@@ -364,7 +364,9 @@ class SitePlan:
         if phi.dim() not in (1, 2) or phi.reshape(phi.shape[0], -1).shape[1] != self.n_out:
             raise ValueError(f"phi must be [S] or [S, {self.n_out}] float64")
         phi = phi.contiguous()
-        total = _result(total, (self.n_out,), torch.float64, self._dev)
+        # the kernel adds into total (callers accumulate several batches)
+        total = torch.zeros(self.n_out, dtype=torch.float64, device=self._dev) if total is None else \
+            _result(total, (self.n_out,), torch.float64, self._dev)
         N.check(N.lib().acedag_reduce_sites(self._h, _vp(phi), phi.shape[0], _vp(total), _stream(phi.device)))
         return total
 

@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--prec", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--alg", default="orig", choices=["orig", "gen"],
+                    help="DAG construction: Algorithm 1 (orig) or Algorithm 2 (gen, insert_generalized)")
+    ap.add_argument("--n", type=int, default=2, help="block size n of Algorithm 2 (--alg gen)")
     ap.add_argument("--sites", type=int, default=None, help="override the config's site count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -84,10 +87,18 @@ def dist_env():
 
 
 # ------------------------------------------------------------- workload
+def with_alg(cfg, alg, n):
+    """The config with its DAG built by Algorithm 2 (graphbuild.py:169-202)
+    instead of Algorithm 1: same targets and coefficients, another node set."""
+    if alg == "orig":
+        return dict(cfg, alg="orig", n=1)
+    return dict(cfg, alg="gen", n=n, sha256=None, desc=cfg["desc"] + f" [Alg. 2 DAG: insert_generalized n={n}]")
+
+
 def workload(cfg, seed=1):
     """The graph (native builder, SHA-pinned) and coefficients [T] / [T, n_out]."""
     import paper_2202_04140_b200 as P
-    g = P.build_graph(P.Group.O3, P.DegreeSpec(1, cfg["D"]), cfg["nu"])
+    g = P.build_graph(P.Group.O3, P.DegreeSpec(1, cfg["D"]), cfg["nu"], cfg.get("alg", "orig"), cfg.get("n", 1))
     rng = np.random.default_rng(seed)
     n_out = cfg["n_out"]
     c = rng.normal(size=len(g.target_ids)) if n_out == 1 else rng.normal(size=(len(g.target_ids), n_out))
@@ -274,9 +285,9 @@ def oracle_workload(cfg, seed=1):
     (graphbuild.py:243-268), SHA-256-checked against the reference's pinned
     hash -- no repo library is loaded on this arm."""
     from oracle import acedag_oracle as O
-    og = O.build_graph("O3", O.Spec(1, cfg["D"]), cfg["nu"])
+    og = O.build_graph("O3", O.Spec(1, cfg["D"]), cfg["nu"], cfg.get("alg", "orig"), cfg.get("n", 1))
     sha = O.graph_sha256(og)
-    if sha != cfg["sha256"]:
+    if cfg["sha256"] and sha != cfg["sha256"]:
         raise SystemExit(f"oracle graph SHA-256 {sha} != pinned {cfg['sha256']}")
     pa, pb, _aux, tg = O.graph_arrays(og)
     rng = np.random.default_rng(seed)
@@ -302,7 +313,7 @@ def run_reference(a):
     if rank != 0:
         return 0
     assert "paper_2202_04140_b200" not in sys.modules
-    cfg = CONFIGS[a.config]
+    cfg = with_alg(CONFIGS[a.config], a.alg, a.n)
     cores = host_cores()
     pa, pb, tg, c, L = oracle_workload(cfg)
     census = dag_census(pa, pb, L, len(tg), cfg, used_seed_count(pa, pb, tg, L))
@@ -333,7 +344,8 @@ def run_reference(a):
                                    input_bytes(cfg, S, L, "f64")),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                              "value_1core": rate1, "cpu_model": cpu_model(),
-                             "graph": "oracle build_graph restatement, SHA-256 == reference " + cfg["sha256"][:16],
+                             "graph": "oracle build_graph restatement" + (
+                                 ", SHA-256 == reference " + cfg["sha256"][:16] if cfg["sha256"] else ""),
                              "sample": cpu_sample_text(cfg, cores, sites // max(1, a.steps)) + f" x {a.steps} steps"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -394,13 +406,15 @@ def run_ours(a):
             return float(t.item())
         return x
 
-    cfg = CONFIGS[a.config]
+    cfg = with_alg(CONFIGS[a.config], a.alg, a.n)
     S, global_sites = shard_sizes(cfg, a.sites or cfg["sites"], rank, world)
     if cfg["scaling"] == "strong":
         lo, hi = shard_range(global_sites, rank, world)
         assert hi - lo == S
     n_out = cfg["n_out"]
     g, c = workload(cfg)
+    import hashlib
+    graph_sha = hashlib.sha256(P.serialize_graph(g)).hexdigest()
     t_plan = time.perf_counter()
     plan = P.SitePlan(g, local).set_coefficients(node_ids=g.target_ids, values=c)
     t_plan = time.perf_counter() - t_plan
@@ -564,7 +578,7 @@ def run_ours(a):
                                    X.numel() * X.element_size()),
             "plan": {"products": info["recursive_products"], "extra_nodes": info["extra_nodes"],
                      "used_seeds": info["used_seeds"], "build_s": round(t_plan, 2),
-                     "graph_sha256": cfg["sha256"]},
+                     "graph_sha256": graph_sha, "graph_sha_pinned": graph_sha == cfg["sha256"] if cfg["sha256"] else None},
             "dag_products_per_s": value * census["P"],
             "naive": naive,
             "roofline": roof,

@@ -255,7 +255,6 @@ struct acedag_plan {
   struct Workspace {
     DevBuf<double> tail;  // split last-round partials
     DevBuf<double2> tiles;  // tile-major seed table (k_tile_seeds)
-    DevBuf<double2> tailc;  // k2_horner TMA staging: per-CTA tail rows
     DevBuf<double2> gcache;
     DevBuf<double2> ws_A;
     DevBuf<double> part;  // K2 partial sums
@@ -827,45 +826,17 @@ template <int NU> struct QuadF64 {
 // k2_horner on the tile-major seed table (V: double2, or float2 for the fp32
 // mode); false (nothing launched) when the input layout is not one
 // tile_seeds knows
-// fp64 k2_horner stages its tiles straight from A (TMA, no tile-major copy);
-// ACEDAG_TMA=0 restores the k_tile_seeds pass (A/B measurements)
-bool horner_tma_enabled() {
-  static bool v = [] {
-    const char* e = getenv("ACEDAG_TMA");
-    return !(e && atoi(e) == 0);
-  }();
-  return v;
-}
-
 template <typename V>
 bool run_horner(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* slot_label, double* out,
                 Launch& lc, cudaStream_t st, cudaError_t& e) {
   constexpr bool f32 = sizeof(V) == 8;
   const acedag_plan::HornerProg& hp = P->hp[f32 ? 1 : 0];
-  if (slot_label != P->slot_label.p && slot_label != P->slot_sorted.p && slot_label != P->slot_identity.p)
-    return false;
+  if (!tile_seeds<128, V>(P, A, S, L, slot_label, lc.ws, st, e)) return false;
+  if (e != cudaSuccess) return true;
+  mark_prep(st);
   const int64_t ntiles = (S + 127) / 128;
   // fewer tiles than SMs: the grid covers program slices of them too
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles * 8, P->sms - t_sm_reserve));
-  HornerTma tma;
-  bool use_tma = !f32 && P->host.max_order <= 4 && horner_tma_enabled() &&
-                 horner_tensor_map(&tma.map, A, S, (int64_t)L);
-  if (use_tma) {
-    // A [S][L] (L: the row length of this input), slot -> column map of the
-    // input layout, one tail cache per CTA
-    const int hot = std::min(P->U, horner_hot_rows(false));
-    const int ntail = std::max(0, P->U - hot - hp.us);
-    e = lc.ws->tailc.alloc(std::max<size_t>(1, (size_t)grid * ntail * 128));
-    if (e != cudaSuccess) return true;
-    tma.A = A;
-    tma.lda = L;
-    tma.col = slot_label;
-    tma.tailc = lc.ws->tailc.p;
-  } else {
-    if (!tile_seeds<128, V>(P, A, S, L, slot_label, lc.ws, st, e)) return false;
-    if (e != cudaSuccess) return true;
-  }
-  mark_prep(st);
   const int nch = nchunks(P);
   e = lc.ws->part.alloc((size_t)grid * nch * 128 * 2);  // double-buffered per CTA
   if (e != cudaSuccess) return true;
@@ -876,9 +847,8 @@ bool run_horner(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
     e = lc.ws->tail.alloc((size_t)(ntiles - full) * nch * 128);
     if (e != cudaSuccess) return true;
   }
-  e = launch_horner(P->host.max_order, f32, use_tma ? nullptr : lc.ws->tiles.p, S, P->U, hp.us, hp.ops.p, hp.chunk.p,
-                    hp.croots.p, nch, out, lc.ws->part.p, full, parts, lc.ws->tail.p, grid, st,
-                    use_tma ? &tma : nullptr);
+  e = launch_horner(P->host.max_order, f32, lc.ws->tiles.p, S, P->U, hp.us, hp.ops.p, hp.chunk.p, hp.croots.p, nch,
+                    out, lc.ws->part.p, full, parts, lc.ws->tail.p, grid, st);
   note_launch();
   mark_main(st);
   if (e != cudaSuccess || parts == 1) return true;

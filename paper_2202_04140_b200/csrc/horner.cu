@@ -20,9 +20,7 @@
 // chunk's per-site partial is stored and the tile's partials are summed in
 // chunk order by warps 0-3 at the start of the CTA's next item (double
 // buffer), so a site's value does not depend on the batch, grid or split.
-#include <cuda.h>
 #include <cuda_runtime.h>
-#include <cudaTypedefs.h>
 #include <stdint.h>
 
 #include <algorithm>
@@ -106,7 +104,7 @@ __device__ __forceinline__ void tmem_st_row(uint32_t addr, const float2 (&v)[4])
            __float_as_uint(v[2].x), __float_as_uint(v[2].y), __float_as_uint(v[3].x), __float_as_uint(v[3].y));
 }
 
-// ----------------------------------------------------------- TMA / mbarrier
+// --------------------------------------------------- bulk copy / mbarrier
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
 }
@@ -124,28 +122,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// one 2-D box of the tensor map into shared memory, completion on bar
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
-      "l"(map), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(c0), "r"(c1)
+// contiguous global -> shared bulk copy on the TMA unit, completion on bar
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
-
-// Where a tile's seed rows come from when the kernel stages them itself
-// (TMA = true): the caller's site-major array A [S][lda] c128, the column of
-// each slot in it, and this kernel's per-CTA cache of tail rows ([rows][128]
-// c128 in global memory, L2-resident) that the warps fill at the tile start.
-struct TileSrc {
-  const double2* A;
-  int64_t lda;
-  const uint16_t* col;  // [U] slot -> column of A
-  double2* tailc;      // [grid][U - hot - us][128]
-};
 
 __device__ __forceinline__ int4 lds128(uint32_t a) {
   int4 r;
@@ -254,10 +236,8 @@ struct SeedsH {
   }
   __device__ __forceinline__ C4<T> gl(uint32_t z) const {
     C4<T> s;
-    // plain (coherent) loads: with TMA staging the tail rows are written by
-    // this CTA during the kernel, which rules out the read-only path
 #pragma unroll
-    for (int k = 0; k < 4; ++k) s.v[k] = *reinterpret_cast<const V*>(gb + z + k * kQ);
+    for (int k = 0; k < 4; ++k) s.v[k] = __ldg(reinterpret_cast<const V*>(gb + z + k * kQ));
     return s;
   }
   __device__ __forceinline__ C4<T> get(uint32_t z, uint32_t cls) const {
@@ -504,17 +484,13 @@ __device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<T
   }
 }
 
-// Seed rows of a tile: TMA = false -- from the tile-major table Tab
-// [ntiles][U + 1][128] (c128 or c64, k_tile_seeds); TMA = true (fp64) --
-// straight from the caller's A: shared-memory rows by TMA box loads
-// (cp.async.bulk.tensor, one [128 sites x 16 B] box per row), TMEM rows and
-// the tail by the warps (the tail into a per-CTA L2-resident cache).
-template <int NU, typename T, bool HYB, int W, bool TMA>
+// Tab: tile-major seed table [ntiles][U + 1][128] (c128 or c64)
+template <int NU, typename T, bool HYB, int W>
 __global__ void __launch_bounds__(W * 32, 1)
 k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, const OpH* __restrict__ ops,
           const int32_t* __restrict__ chunk, const int32_t* __restrict__ croots, int nchunk,
           double* __restrict__ out, double* __restrict__ part, int64_t full_tiles, int tail_parts,
-          double* __restrict__ tailbuf, const __grid_constant__ CUtensorMap tmA, TileSrc src) {
+          double* __restrict__ tailbuf) {
   using V = typename HTr<T>::V;
   constexpr int kC = HTr<T>::kCols;
   constexpr uint32_t kRow = HTr<T>::kRow;
@@ -527,14 +503,11 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
   const uint32_t rings = sbase + (uint32_t)us * kRow;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + (size_t)us * kRow + W * kHornerRing);
   int* dyn = reinterpret_cast<int*>(tslot) + 1;
-  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(tslot) + 8;  // TMA completion (8 B aligned)
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(tslot) + 8;  // bulk-copy completion (8 B aligned)
   uint32_t bar_phase = 0;
-  const int ntail = U - hot - us;  // rows past the on-chip ones (HYB)
-  if constexpr (TMA) {
-    if (threadIdx.x == 0) {
-      mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
@@ -558,11 +531,11 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
   double* mypart0 = part + (size_t)blockIdx.x * nchunk * 128 * 2;
   int pbuf = 0;
   int64_t pend_tile = -1;
-  auto sum_tile = [&](int64_t t, const double* prt) {
+  auto sum_tile = [&](int64_t t, const double* src) {
     const int i = threadIdx.x;  // warps 0-3: site t * 128 + i
     double s = 0.0;
 #pragma unroll 16
-    for (int ci = 0; ci < nchunk; ++ci) s += __ldcg(prt + (size_t)ci * 128 + i);
+    for (int ci = 0; ci < nchunk; ++ci) s += __ldcg(src + (size_t)ci * 128 + i);
     const int64_t site = t * 128 + i;
     if (site < S) out[site] = s;
   };
@@ -576,109 +549,51 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
     const int nsl = whole ? 1 : tail_parts;
     const int cb = (int)((int64_t)slice * nchunk / nsl), ce = (int)((int64_t)(slice + 1) * nchunk / nsl);
     const V* Tt = Tab + tile * (int64_t)rows * 128;
-    if constexpr (TMA) {
-      // shared-memory rows: one TMA box per row, sites past S zero-filled;
-      // the previous item's generic reads of these rows ended at the barrier
-      if (threadIdx.x == 0 && us > 0) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        mbar_expect_tx(bar, (uint32_t)us * kRow);
-        for (int r = 0; r < us; ++r)
-          tma_load_2d(sbase + (uint32_t)r * kRow, &tmA, 2 * __ldg(src.col + hot + r), (int)(tile * 128), bar);
-      }
-      // TMEM rows: each lane loads its four sites of a row straight from A
-      const double2* Arow[4];
-      bool ok[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t site = tile * 128 + k * 32 + lane;
-        ok[k] = site < S;
-        Arow[k] = src.A + (ok[k] ? site : 0) * src.lda;
-      }
-      for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (W / 4)) {
-        V v[4][4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int h = h0 + q * (W / 4);
-          const int c = h < hot ? __ldg(src.col + h) : 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            v[q][k] = (h < hot && ok[k]) ? ld_stream(reinterpret_cast<const V*>(Arow[k] + c)) : mk2(T(0), T(0));
+    // the next item's on-chip rows into L2 while this tile computes
+    if (threadIdx.x == 0 && it + gridDim.x < nitems) {
+      const int64_t nit = it + gridDim.x;
+      const int64_t nt = nit < full_tiles ? nit : full_tiles + (nit - full_tiles) / tail_parts;
+      if (nt != tile) {
+        const char* src = reinterpret_cast<const char*>(Tab + nt * (int64_t)rows * 128);
+        const uint32_t bytes = (uint32_t)(hot + us) * kRow;
+        for (uint32_t o = 0; o < bytes; o += 32768u) {
+          const uint32_t n = bytes - o < 32768u ? bytes - o : 32768u;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src + o), "r"(n) : "memory");
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int h = h0 + q * (W / 4);
-          if (h < hot) tmem_st_row(sd.tq + (uint32_t)(h * kC), v[q]);
-        }
-      }
-      // the tail: copied once per tile into this CTA's cache (contiguous
-      // 2 KB rows, so a tail fetch reads 512 B per site group, not 32 rows)
-      if (HYB) {
-        V* cache = reinterpret_cast<V*>(src.tailc) + (size_t)blockIdx.x * ntail * 128;
-        sd.gb = reinterpret_cast<const char*>(cache) + lane * sizeof(V);
-        for (int t0 = warp; t0 < ntail; t0 += 4 * W) {
-          V v[4][4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int t = t0 + q * W;
-            const int c = t < ntail ? __ldg(src.col + hot + us + t) : 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              v[q][k] = (t < ntail && ok[k]) ? ld_stream(reinterpret_cast<const V*>(Arow[k] + c)) : mk2(T(0), T(0));
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int t = t0 + q * W;
-            if (t < ntail)
-#pragma unroll
-              for (int k = 0; k < 4; ++k) cache[(size_t)t * 128 + k * 32 + lane] = v[q][k];
-          }
-        }
-      }
-      if (us > 0) {
-        mbar_wait(bar, bar_phase);
-        bar_phase ^= 1;
-      }
-    } else {
-      // the next item's on-chip rows into L2 while this tile computes
-      if (threadIdx.x == 0 && it + gridDim.x < nitems) {
-        const int64_t nit = it + gridDim.x;
-        const int64_t nt = nit < full_tiles ? nit : full_tiles + (nit - full_tiles) / tail_parts;
-        if (nt != tile) {
-          const char* nxt = reinterpret_cast<const char*>(Tab + nt * (int64_t)rows * 128);
-          const uint32_t bytes = (uint32_t)(hot + us) * kRow;
-          for (uint32_t o = 0; o < bytes; o += 32768u) {
-            const uint32_t n = bytes - o < 32768u ? bytes - o : 32768u;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(nxt + o), "r"(n) : "memory");
-          }
-        }
-      }
-      if (HYB) sd.gb = reinterpret_cast<const char*>(Tt + (size_t)(hot + us) * 128) + lane * sizeof(V);
-      // TMEM rows: each lane quadrant's W/4 warps write all hot rows
-      for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (W / 4)) {
-        V v[4][4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int h = h0 + q * (W / 4);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) v[q][k] = h < hot ? ld_stream(Tt + (size_t)h * 128 + k * 32 + lane) : mk2(T(0), T(0));
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int h = h0 + q * (W / 4);
-          if (h < hot) tmem_st_row(sd.tq + (uint32_t)(h * kC), v[q]);
-        }
-      }
-      // shared rows: asynchronous 16-byte copies
-      {
-        const char* rowsrc = reinterpret_cast<const char*>(Tt + (size_t)hot * 128);
-        const int n16 = us * (int)(kRow / 16);
-        for (int idx = threadIdx.x; idx < n16; idx += W * 32)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + idx * 16), "l"(rowsrc + (size_t)idx * 16)
-                       : "memory");
       }
     }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    // shared rows: the tile's us rows are contiguous in the table, so one
+    // elected thread moves them with TMA bulk copies (cp.async.bulk, 64 KB
+    // pieces) completing on an mbarrier while the warps fill TMEM below; the
+    // previous item's generic reads of these rows ended at its barrier
+    if (threadIdx.x == 0 && us > 0) {
+      const char* src = reinterpret_cast<const char*>(Tt + (size_t)hot * 128);
+      const uint32_t bytes = (uint32_t)us * kRow;
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_expect_tx(bar, bytes);
+      for (uint32_t o = 0; o < bytes; o += 65536u)
+        bulk_g2s(sbase + o, src + o, bytes - o < 65536u ? bytes - o : 65536u, bar);
+    }
+    if (HYB) sd.gb = reinterpret_cast<const char*>(Tt + (size_t)(hot + us) * 128) + lane * sizeof(V);
+    // TMEM rows: each lane quadrant's W/4 warps write all hot rows
+    for (int h0 = warp >> 2; h0 < hot; h0 += 4 * (W / 4)) {
+      V v[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int h = h0 + q * (W / 4);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[q][k] = h < hot ? ld_stream(Tt + (size_t)h * 128 + k * 32 + lane) : mk2(T(0), T(0));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int h = h0 + q * (W / 4);
+        if (h < hot) tmem_st_row(sd.tq + (uint32_t)(h * kC), v[q]);
+      }
+    }
+    if (us > 0) {
+      mbar_wait(bar, bar_phase);
+      bar_phase ^= 1;
+    }
     if (threadIdx.x == 0) *dyn = cb + W;
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -979,36 +894,30 @@ bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::
 template <int NU, typename T, bool HYB>
 static cudaError_t launch_nu(const void* Tab, int64_t S, int U, int us, const OpH* ops, const int32_t* chunk,
                              const int32_t* croots, int nchunk, double* out, double* part, int64_t full, int parts,
-                             double* tail, int grid, cudaStream_t st, const HornerTma* tma) {
+                             double* tail, int grid, cudaStream_t st) {
   const int W = horner_warps(sizeof(T) == 4, NU);
-  auto k = hdev::k2_horner<NU, T, HYB, 16, false>;
+  auto k = hdev::k2_horner<NU, T, HYB, 16>;
   if constexpr (sizeof(T) == 4) {
-    if (W == 32) k = hdev::k2_horner<NU, T, HYB, 32, false>;
-  } else if constexpr (NU <= 4) {
-    if (tma) k = hdev::k2_horner<NU, T, HYB, 16, true>;
+    if (W == 32) k = hdev::k2_horner<NU, T, HYB, 32>;
   }
   const size_t smem = horner_smem(us, sizeof(T) == 4, NU);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  static const CUtensorMap kNoMap{};
-  hdev::TileSrc src{nullptr, 0, nullptr, nullptr};
-  if (tma) src = hdev::TileSrc{static_cast<const double2*>(tma->A), tma->lda, tma->col, static_cast<double2*>(tma->tailc)};
   k<<<grid, W * 32, smem, st>>>(reinterpret_cast<const typename hdev::HTr<T>::V*>(Tab), S, U, us, ops, chunk, croots,
-                                nchunk, out, part, full, parts, tail, tma ? tma->map : kNoMap, src);
+                                nchunk, out, part, full, parts, tail);
   return cudaGetLastError();
 }
 
 cudaError_t launch_horner(int nu, bool f32, const void* Tab, int64_t S, int U, int us, const OpH* ops,
                           const int32_t* chunk, const int32_t* croots, int nchunk, double* out, double* part,
-                          int64_t full, int parts, double* tail, int grid, cudaStream_t st, const HornerTma* tma) {
+                          int64_t full, int parts, double* tail, int grid, cudaStream_t st) {
   const int hot = std::min(U, horner_hot_rows(f32));
   const bool hyb = hot + us < U;
-  if (tma && (f32 || nu > 4)) return cudaErrorInvalidValue;
 #define ACEDAG_H(N, T)                                                                                          \
   return hyb ? launch_nu<N, T, true>(Tab, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail,  \
-                                     grid, st, tma)                                                           \
+                                     grid, st)                                                                \
              : launch_nu<N, T, false>(Tab, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail, \
-                                      grid, st, tma)
+                                      grid, st)
   if (f32) {
     switch (nu) {
       case 2: ACEDAG_H(2, float);
@@ -1028,27 +937,6 @@ cudaError_t launch_horner(int nu, bool f32, const void* Tab, int64_t S, int U, i
     default: return cudaErrorInvalidValue;
   }
 #undef ACEDAG_H
-}
-
-// the tensor map of a site-major c128 array [S][lda] seen as doubles
-// [S][2 lda], one box = 128 sites x one column (16 B); sites past S read 0
-bool horner_tensor_map(CUtensorMap* map, const void* A, int64_t S, int64_t lda) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }();
-  if (!encode || S < 1 || lda < 1 || S > ((int64_t)1 << 31) || 2 * lda > ((int64_t)1 << 31)) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)(2 * lda), (cuuint64_t)S};
-  const cuuint64_t strides[1] = {(cuuint64_t)lda * 16};
-  const cuuint32_t box[2] = {2, 128};
-  const cuuint32_t estr[2] = {1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(A), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace acedag

@@ -14,7 +14,6 @@
 #include <cstdint>
 #include <vector>
 
-#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "plan.h"
@@ -56,24 +55,10 @@ bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::
 int horner_us_max(size_t smem_optin, bool f32, int nu);
 size_t horner_smem(int us, bool f32, int nu);
 
-// fp64 seed staging straight from the caller's array (no tile-major table):
-// the TMA descriptor of A (horner_tensor_map), A itself [S][lda] c128, the
-// column of every slot, and a per-CTA tail cache [grid][U - hot - us][128] c128
-struct HornerTma {
-  CUtensorMap map;
-  const void* A;
-  int64_t lda;
-  const uint16_t* col;
-  void* tailc;
-};
-bool horner_tensor_map(CUtensorMap* map, const void* A, int64_t S, int64_t lda);
-
-// tiles: tile-major seed table [ntiles][U+1][128] c128 / c64 (k_tile_seeds<128>),
-// unused when tma is given (fp64, order <= 4).
+// tiles: tile-major seed table [ntiles][U+1][128] c128 / c64 (k_tile_seeds<128>).
 // part: [grid][2][nchunk][128]; tail: [(ntiles - full)][nchunk][128].
 cudaError_t launch_horner(int nu, bool f32, const void* tiles, int64_t S, int U, int us, const OpH* ops,
                           const int32_t* chunk, const int32_t* croots, int nchunk, double* out, double* part,
-                          int64_t full, int parts, double* tail, int grid, cudaStream_t st,
-                          const HornerTma* tma = nullptr);
+                          int64_t full, int parts, double* tail, int grid, cudaStream_t st);
 
 }  // namespace acedag

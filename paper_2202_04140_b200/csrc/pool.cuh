@@ -349,14 +349,20 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
   double* WR = reinterpret_cast<double*>(Y + NB * NPp);                 // [NB][C1]
   const double inv_span = 1.0 / (r_cut - r_in);
   int tq[TPL];  // this lane's triples: pair << 8 | n (-1: none)
+  // output columns of each triple and of its m -> -m partner (-1: not
+  // wanted), looked up once: the site loop then stores without dependent
+  // global loads
+  int cpos[TPL], cneg[TPL];
 #pragma unroll
   for (int t = 0; t < TPL; ++t) {
     const int i = lane + 32 * t;
+    tq[t] = -1;
+    cpos[t] = cneg[t] = -1;
     if (i < ntri) {
       const int4 q = __ldg(tri + i);
       tq[t] = (q.y * (q.y + 1) / 2 + q.z) << 8 | q.x;
-    } else {
-      tq[t] = -1;
+      cpos[t] = col_of ? col_of[q.w] : q.w;
+      if (q.z > 0) cneg[t] = (col_of ? col_of[q.w - 2 * q.z] : q.w - 2 * q.z) | (q.z & 1) << 30;
     }
   }
   for (int64_t s = (int64_t)blockIdx.x * W + warp; s < S; s += (int64_t)gridDim.x * W) {
@@ -438,16 +444,11 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
     }
 #pragma unroll
     for (int t = 0; t < TPL; ++t) {
-      if (tq[t] >= 0) {
-        const int4 q = __ldg(tri + lane + 32 * t);
-        const int cpos = col_of ? col_of[q.w] : q.w;
-        if (cpos >= 0) out[s * out_stride + cpos] = acc[t];
-        if (q.z > 0) {  // A[n, l, -m] = (-1)^m conj(A[n, l, m])
-          const int lab_m = q.w - 2 * q.z;
-          const int cm = col_of ? col_of[lab_m] : lab_m;
-          const double sg = (q.z & 1) ? -1.0 : 1.0;
-          if (cm >= 0) out[s * out_stride + cm] = make_double2(sg * acc[t].x, -sg * acc[t].y);
-        }
+      if (cpos[t] >= 0) out[s * out_stride + cpos[t]] = acc[t];
+      const int cm = cneg[t] & 0x3FFFFFFF;
+      if (cneg[t] >= 0 && cm != 0x3FFFFFFF) {  // A[n, l, -m] = (-1)^m conj(A[n, l, m])
+        const double sg = (cneg[t] >> 30) & 1 ? -1.0 : 1.0;
+        out[s * out_stride + cm] = make_double2(sg * acc[t].x, -sg * acc[t].y);
       }
     }
   }

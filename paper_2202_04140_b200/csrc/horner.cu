@@ -290,10 +290,20 @@ __device__ __forceinline__ void cmac(C4<T>& Hp, const C4<T>& s, const C4<T>& H) 
   }
 }
 
+// inner records: w = nch | nhot << 15 | nsm << 22 (children counts by class)
 __device__ __forceinline__ uint32_t w_nch(uint32_t w) { return w & 0x7FFFu; }
 __device__ __forceinline__ uint32_t w_nhot(uint32_t w) { return (w >> 15) & 127u; }
 __device__ __forceinline__ uint32_t w_nsm(uint32_t w) { return w >> 22; }
-constexpr uint32_t kOneHot = 1u | 1u << 15, kTwoHot = 2u | 2u << 15;
+// a node of the last inner order (its children are leaves, <= kMaxLeaves):
+// w = the byte ends of its hot / shared / all leaf records past the first
+// leaf, 10 bits each, so the leaf loops need no count arithmetic
+__device__ __forceinline__ uint32_t lw_hot(uint32_t w) { return w & 1023u; }
+__device__ __forceinline__ uint32_t lw_sm(uint32_t w) { return (w >> 10) & 1023u; }
+__device__ __forceinline__ uint32_t lw_end(uint32_t w) { return w >> 20; }
+constexpr uint32_t leaf_word(uint32_t n, uint32_t nh, uint32_t ns) {
+  return nh * 16 | (nh + ns) * 16 << 10 | n * 16 << 20;
+}
+constexpr uint32_t kOneHot = leaf_word(1, 1, 0), kTwoHot = leaf_word(2, 2, 0);
 
 // ---------------------------------------------------------------- program walk
 template <uint32_t PC, typename T, bool HYB>
@@ -336,15 +346,14 @@ __device__ __forceinline__ void hot_leaves(uint32_t q, uint32_t qh, C4<T>& H, co
 // other loops.
 template <typename T, bool HYB>
 __device__ __forceinline__ void leaves(uint32_t q, uint32_t w, T c, int4 l, C4<T>& H, const SeedsH<T, HYB>& sd) {
-  const uint32_t nh = w_nhot(w), ns = w_nsm(w), n = w_nch(w);
-  const uint32_t qh = q + nh * 16, qs = qh + ns * 16, qe = q + n * 16;
-  if (nh) {
+  const uint32_t qh = q + lw_hot(w), qs = q + lw_sm(w), qe = q + lw_end(w);
+  if (qh != q) {
     axpy_init(H, c, rec_c<T>(l), seed_of<0>(sd, (uint32_t)l.z));
     hot_leaves(q + 16, qh, H, sd);
-    if (nh == n) return;
+    if (qh == qe) return;
     q = qh;
-  } else if (n) {
-    axpy_init(H, c, rec_c<T>(l), ns ? sd.sm((uint32_t)l.z) : sd.gl((uint32_t)l.z));
+  } else if (qe != q) {
+    axpy_init(H, c, rec_c<T>(l), qs != q ? sd.sm((uint32_t)l.z) : sd.gl((uint32_t)l.z));
     q += 16;
   } else {
     init_h(H, c);
@@ -409,7 +418,7 @@ __device__ __forceinline__ void parents(RingH& st, uint32_t n, C4<T>& Hp, const 
     }
     if constexpr (PC != 0) sp = seed_of<PC>(sd, (uint32_t)r.z);
     cmac(Hp, sp, H);
-    st.p += 16 * (1 + w_nch(w));
+    st.p += 16 + lw_end(w);
     st.check(lane);
   }
 }
@@ -456,7 +465,7 @@ __device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<T
   C4<T> H;
   if constexpr (NU == 3) {
     leaves(st.p + 32, (uint32_t)r0.w, c, st.at(2), H, sd);
-    st.p += 16 * (2 + w_nch((uint32_t)r0.w));
+    st.p += 32 + lw_end((uint32_t)r0.w);
     st.check(lane);
   } else {
     init_h(H, c);
@@ -658,7 +667,6 @@ size_t horner_smem(int us, bool f32, int nu) {
 }
 
 namespace {
-uint32_t w_count(uint32_t w) { return w & 0x7FFFu; }
 // relative size of the second half of the chunks (ACEDAG_HGUIDE; 1 = equal)
 double guided_tail() {
   static double v = [] {
@@ -724,10 +732,11 @@ struct HornerEnc {
       cls_rec.push_back((uint8_t)cls(slot(l)));
     }
   }
+  // the record word of a node whose children are leaves (hdev::leaf_word)
   uint32_t leaf_w(const std::vector<size_t>& kids, size_t b, size_t e) {
     uint32_t n = 0, nh = 0, ns = 0;
     for (size_t j = b; j < e; ++j) count(cls(slot(H.ops[kids[j]])), 1, n, nh, ns);
-    return pack(n, nh, ns);
+    return hdev::leaf_word(n, nh, ns);
   }
   std::vector<size_t> kids_of(size_t pos) const { return kids_from(pos + 1, H.ops[pos].nch); }
   std::vector<size_t> kids_from(size_t q, uint32_t n) const {
@@ -838,7 +847,8 @@ bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::
       // the units the root became (a split NU=3 root: consecutive pair + leaves)
       size_t q = b0;
       for (int32_t k = r0; k < E.nroots; ++k) {
-        const size_t e = E.nroots - r0 == 1 ? out.size() : q + 2 + w_count(out[q].w);
+        // a split order-3 root is its pair + leaves (leaf word: n leaves at w >> 24)
+        const size_t e = E.nroots - r0 == 1 ? out.size() : q + 2 + (out[q].w >> 24);
         start.push_back(q);
         double c = cost_w(2);
         for (size_t t = q; t < e; ++t)

@@ -107,21 +107,24 @@ def simulate_horner(h, A):
         assert (cls == 1 and s < hot + us) or (cls == 2 and s >= hot + us)
         return seeds[:, s]
 
-    def cls_of(j, w):
+    def cls_of(j, w):  # inner record: counts nch | nhot << 15 | nsm << 22
         nh, ns = (w >> 15) & 127, w >> 22
         return 0 if j < nh else (1 if j < nh + ns else 2)
+
+    def leaf_cls(j, w):  # last inner order: byte ends hot | shared << 10 | all << 20
+        return 0 if 16 * j < (w & 1023) else (1 if 16 * j < ((w >> 10) & 1023) else 2)
 
     pos = 0
 
     def leaves(w, H):
         nonlocal pos
-        n = w & 0x7FFF
-        assert n <= HORNER_MAX_LEAVES
+        n = (w >> 20) // 16
+        assert (w >> 20) % 16 == 0 and n <= HORNER_MAX_LEAVES
         for j in range(n):
             r = ops[pos]
             pos += 1
             assert r["w"] == 0
-            H = H + r["c"] * seed(r["z"], cls_of(j, w))
+            H = H + r["c"] * seed(r["z"], leaf_cls(j, w))
         return H
 
     def children(w, D, Hp):

@@ -548,15 +548,19 @@ def run_ours(a):
     roof["kernel_ms"] = ms_step if pos else k2_ms
     roof["step_share"] = roof["kernel_ms"] / ms_step
     roof["phases_ms"] = phases
-    prof = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    # DRAM bytes of the same kernel on the same workload from the committed
+    # ncu --set full capture (only when kernel and site count match this run)
     roof["traffic"] = None
-    if os.path.exists(prof):
-        try:
-            ent = json.load(open(prof)).get(a.config)
-            if ent and ent.get("kernel") == roof.get("kernel"):
-                roof["traffic"] = ent["bytes"]
-        except Exception:
-            pass
+    for rnd in ("r02", "r01"):
+        prof = os.path.join(ROOT, "profiles", rnd, "traffic.json")
+        if roof["traffic"] is None and os.path.exists(prof) and a.alg == "orig" and a.prec == "f64":
+            try:
+                ent = json.load(open(prof)).get(a.config)
+                if ent and ent.get("kernel") == roof.get("kernel") and ent.get("sites", S) == S:
+                    roof["traffic"] = ent["bytes"]
+                    roof["traffic_source"] = ent.get("source", prof)
+            except Exception:
+                pass
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

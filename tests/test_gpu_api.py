@@ -227,3 +227,38 @@ def test_device_entry_points_validate_tensors(cuda):
     big = P.pool_batched(P.Group.O3, 3, coords, torch.tensor([99, 3], dtype=torch.int32, device=cuda))
     full = P.pool_batched(P.Group.O3, 3, coords)
     assert torch.equal(big, full)
+
+
+def test_pool_keys_cover_seeds(cuda):  # test_evaluator.py:85-89
+    spec = DegreeSpec(1, 4)
+    g = P.seed_graph(Group.SO2, spec)
+    pooled = P.pool(Group.SO2, spec, [(0.5, 1.0)])
+    assert set(pooled) == {n.elements[0] for n in g.nodes}
+
+
+def test_multiplication_count_below_naive():  # test_evaluator.py:128-137 (host only)
+    for numax in (3, 4, 5):
+        g = P.build_graph(Group.T, DegreeSpec(1, 10), numax)
+        graph_muls = sum(1 for node in g.nodes if node.order >= 2)
+        naive_muls = sum(node.order - 1 for node in g.nodes if not node.auxiliary and g.is_target(node.elements))
+        assert graph_muls < naive_muls
+
+
+def test_invariance_negative_control(cuda):  # test_evaluator.py:214-222
+    spec = DegreeSpec(1, 3)
+    parts = [(0.0,), (0.5,), (1.2,)]
+    before = P.naive_eval(T(1, 1), P.pool(Group.T, spec, parts))
+    after = P.naive_eval(T(1, 1), P.pool(Group.T, spec, P.rotate_particles(Group.T, parts, math.pi / 2)))
+    assert dev(after, before) > 1e-2
+    assert after == pytest.approx(-before)  # phase e^(i pi)
+
+
+def test_conjugation_of_negated_tuple(cuda):  # test_evaluator.py:224-233
+    g = P.build_graph(Group.T, DegreeSpec(1, 6), 3)
+    parts = [(0.4,), (1.9,), (2.7,)]
+    vals = P.evaluate_graph(g, P.pool(Group.T, g.spec, parts))
+    for node in g.nodes:
+        if node.auxiliary or not g.is_target(node.elements):
+            continue
+        negated = canonical((-m,) for (m,) in node.elements)
+        assert vals[g.id_of(negated)] == pytest.approx(vals[node.id].conjugate(), abs=1e-12)

@@ -87,3 +87,44 @@ def test_rotation_is_azimuthal():
     parts = [(0.5, 1.0, 2.0, 0.25)]
     assert P.rotate_particles(P.Group.O3F, parts, 0.5) == [(0.5, 1.0, 2.5, 0.25)]
     assert P.invert_particles(P.Group.O3F, parts) == [(0.5, math.pi - 1.0, 2.0 + math.pi, 0.25)]
+
+
+class TestParticleFiles:  # reference tests/test_evaluator.py:240-265, restated
+    def test_roundtrip(self, tmp_path):
+        parts = [(0.5, 1.0, 2.0, -0.25), (0.1, 0.2, 0.3, 0.4)]
+        path = tmp_path / "conf.txt"
+        P.write_particles(path, P.Group.O3F, parts)
+        group, got = P.read_particles(path)
+        assert group is P.Group.O3F and got == parts
+
+    def test_missing_header(self, tmp_path):
+        path = tmp_path / "conf.txt"
+        path.write_text("0.1 0.2\n")
+        with pytest.raises(ValueError):
+            P.read_particles(path)
+
+    def test_bad_line(self, tmp_path):
+        path = tmp_path / "conf.txt"
+        path.write_text("# group=T\nnot-a-number\n")
+        with pytest.raises(ValueError):
+            P.read_particles(path)
+
+    def test_empty_config(self, tmp_path):
+        path = tmp_path / "conf.txt"
+        P.write_particles(path, P.Group.T, [])
+        group, got = P.read_particles(path)
+        assert group is P.Group.T and got == []
+
+
+class TestCoefficientFiles:  # reference tests/test_evaluator.py:268-279, restated
+    def test_roundtrip(self, tmp_path):
+        coeffs = {((-1,), (1,)): 1.5 + 0.5j, ((0,),): -2.0 + 0j}
+        path = tmp_path / "c.txt"
+        P.write_coefficients(path, coeffs)
+        assert P.read_coefficients(path, P.Group.T) == coeffs
+
+    def test_bad_line(self, tmp_path):
+        path = tmp_path / "c.txt"
+        path.write_text("-1,1 1.0\n")
+        with pytest.raises(ValueError):
+            P.read_coefficients(path, P.Group.T)

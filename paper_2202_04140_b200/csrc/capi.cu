@@ -1331,7 +1331,8 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
   static const bool force_v2 = getenv("ACEDAG_POOL") && atoi(getenv("ACEDAG_POOL")) == 2;
   bool done = false;
   if (!force_v2 && (cap == 12 || cap == 14) && ntri <= 32 * 16) {
-    auto launch4 = [&](auto k, int W, size_t sm4) -> cudaError_t {
+    auto launch4 = [&](auto k, int W, size_t wb) -> cudaError_t {
+      const size_t sm4 = (size_t)W * wb;
       cudaError_t e4 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);
       if (e4 != cudaSuccess) return e4;
       const int g4 = (int)std::min<int64_t>((S + W - 1) / W, (int64_t)sms * 64);
@@ -1340,11 +1341,11 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
     };
     cudaError_t e4;
     if (cap == 12)
-      e4 = ntri <= 256 ? launch4(dev::pool_positions4<12, 8>, dev::Pool4Geom<12>::kW, dev::Pool4Geom<12>::kSmem)
-                       : launch4(dev::pool_positions4<12, 16>, dev::Pool4Geom<12>::kW, dev::Pool4Geom<12>::kSmem);
+      e4 = ntri <= 256 ? launch4(dev::pool_positions4<12, 8>, dev::Pool4Geom<12>::kW, dev::Pool4Geom<12>::kWarpBytes)
+                       : launch4(dev::pool_positions4<12, 16>, dev::Pool4Geom<12>::kW, dev::Pool4Geom<12>::kWarpBytes);
     else
-      e4 = ntri <= 256 ? launch4(dev::pool_positions4<14, 8>, dev::Pool4Geom<14>::kW, dev::Pool4Geom<14>::kSmem)
-                       : launch4(dev::pool_positions4<14, 16>, dev::Pool4Geom<14>::kW, dev::Pool4Geom<14>::kSmem);
+      e4 = ntri <= 256 ? launch4(dev::pool_positions4<14, 8>, dev::Pool4Geom<14>::kW, dev::Pool4Geom<14>::kWarpBytes)
+                       : launch4(dev::pool_positions4<14, 16>, dev::Pool4Geom<14>::kW, dev::Pool4Geom<14>::kWarpBytes);
     note_launch();
     if (e4 != cudaSuccess) return cuda_fail(e4, "pool_positions4");
     done = true;

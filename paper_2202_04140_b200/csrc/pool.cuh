@@ -325,7 +325,9 @@ namespace dev {
 // into shared memory Y[j][pair] (row stride odd in 16-B units: conflict-free
 // for both the lane = j writes and the lane = triple reads).  Then every
 // lane accumulates its TPL (n, l, m >= 0) triples A = sum_j WR[j][n] Y[j][lm]
-// in registers, j ascending, NB neighbours per pass.
+// in registers, j ascending, NB neighbours per pass.  (Round 2: splitting
+// each neighbour's table over two lanes by the parity of m, so every lane
+// works in the table phase, ran 2.1 vs 1.92 ms per 131k-site cfg3 chunk.)
 template <int CAP, int NB = 16>
 struct Pool4Geom {
   static constexpr int kNB = NB;  // neighbours per pass (lanes computing Y)
@@ -333,13 +335,11 @@ struct Pool4Geom {
   static constexpr int kNP = kC1 * (CAP + 2) / 2;
   static constexpr int kNPp = kNP | 1;  // odd stride (16-B units)
   static constexpr size_t kWarpBytes = (size_t)NB * kNPp * 16 + (size_t)NB * kC1 * 8;
-  // warps per CTA: the per-warp tables and the shared norm table in 227 KB
-  static constexpr int kW = (int)((227 * 1024 - kNP * 8) / kWarpBytes) < 16 ? (int)((227 * 1024 - kNP * 8) / kWarpBytes) : 16;
-  static constexpr size_t kSmem = (size_t)kW * kWarpBytes + (size_t)kNP * 8;
+  static constexpr int kW = (int)((227 * 1024) / kWarpBytes) < 16 ? (int)((227 * 1024) / kWarpBytes) : 16;
 };
 
 template <int CAP, int TPL>
-__global__ void __launch_bounds__(Pool4Geom<CAP>::kW * 32, 1)
+__global__ void __launch_bounds__(Pool4Geom<CAP>::kW * 32)
 pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ counts, int64_t S, int J, double r_in,
                 double r_cut, const int4* __restrict__ tri, int ntri, const int32_t* __restrict__ col_of,
                 int64_t out_stride, double2* __restrict__ out) {
@@ -349,21 +349,22 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* Y = reinterpret_cast<double2*>(psm + G::kWarpBytes * warp);  // [NB][NPp]
   double* WR = reinterpret_cast<double*>(Y + NB * NPp);                 // [NB][C1]
-  // the Y_lm norms in shared memory: the two lanes of a neighbour index
-  // different m, which a constant-bank load would serialise
-  double* s_norm = reinterpret_cast<double*>(psm + G::kWarpBytes * W);
-  for (int i = threadIdx.x; i < G::kNP; i += blockDim.x) s_norm[i] = c_ylm_norm[i];
-  __syncthreads();
   const double inv_span = 1.0 / (r_cut - r_in);
   int tq[TPL];  // this lane's triples: pair << 8 | n (-1: none)
+  // output columns of each triple and of its m -> -m partner (-1: not
+  // wanted), looked up once: the site loop then stores without dependent
+  // global loads
+  int cpos[TPL], cneg[TPL];
 #pragma unroll
   for (int t = 0; t < TPL; ++t) {
     const int i = lane + 32 * t;
+    tq[t] = -1;
+    cpos[t] = cneg[t] = -1;
     if (i < ntri) {
       const int4 q = __ldg(tri + i);
       tq[t] = (q.y * (q.y + 1) / 2 + q.z) << 8 | q.x;
-    } else {
-      tq[t] = -1;
+      cpos[t] = col_of ? col_of[q.w] : q.w;
+      if (q.z > 0) cneg[t] = (col_of ? col_of[q.w - 2 * q.z] : q.w - 2 * q.z) | (q.z & 1) << 30;
     }
   }
   for (int64_t s = (int64_t)blockIdx.x * W + warp; s < S; s += (int64_t)gridDim.x * W) {
@@ -373,20 +374,15 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
     for (int t = 0; t < TPL; ++t) acc[t] = make_double2(0.0, 0.0);
     for (int j0 = 0; j0 < nj; j0 += NB) {
       const int nb = min(NB, nj - j0);
-      // two lanes per neighbour: lane j and j + NB share neighbour j, the
-      // first also writes its radial row; both walk the e^{im phi} and
-      // P_m^m recurrences one m at a time (the same operations as a single
-      // lane) and each runs the upward l-recursion for its own parity of m
-      const int jl = lane % NB, half = lane / NB;
-      if (jl < nb) {
-        const double* p = xyz + (s * J + j0 + jl) * 3;
+      if (lane < nb) {
+        const double* p = xyz + (s * J + j0 + lane) * 3;
         const double x = p[0], y = p[1], z = p[2];
         const double rho2 = x * x + y * y;
         const double r = sqrt(rho2 + z * z);
-        if (half == 0) {
-          const double w = r < r_cut ? 0.5 * (1.0 + cospi(r / r_cut)) : 0.0;
-          const double u = 2.0 * fmin(1.0, fmax(0.0, (r - r_in) * inv_span)) - 1.0;
-          double* wr = WR + jl * C1;
+        const double w = r < r_cut ? 0.5 * (1.0 + cospi(r / r_cut)) : 0.0;
+        const double u = 2.0 * fmin(1.0, fmax(0.0, (r - r_in) * inv_span)) - 1.0;
+        double* wr = WR + lane * C1;
+        {
           double t0 = 1.0, t1 = u;
           wr[0] = w;
           if (CAP >= 1) wr[1] = w * u;
@@ -401,49 +397,29 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
         const double rho = sqrt(rho2);
         const double ct = r > 0.0 ? z / r : 1.0, st = r > 0.0 ? rho / r : 0.0;
         const double cp = rho > 0.0 ? x / rho : 1.0, sp = rho > 0.0 ? y / rho : 0.0;
-        double2* yj = Y + jl * NPp;
+        double2* yj = Y + lane * NPp;
         double ec = 1.0, es = 0.0, pmm = 1.0;
-        if (half) {  // the m = 1 step of the single-lane walk
-          ec = cp;
-          es = sp;
-          pmm *= -st;
-        }
 #pragma unroll
-        for (int k = 0; 2 * k <= CAP; ++k) {
-          const int m = 2 * k + half;
-          if (k > 0) {
-#pragma unroll
-            for (int d = 1; d >= 0; --d) {  // to m - 1, then to m
-              const double mm = (double)(m - d);
-              const double nc = ec * cp - es * sp;
-              es = ec * sp + es * cp;
-              ec = nc;
-              pmm *= -(2.0 * mm - 1.0) * st;
-            }
+        for (int m = 0; m <= CAP; ++m) {
+          if (m > 0) {
+            const double nc = ec * cp - es * sp;
+            es = ec * sp + es * cp;
+            ec = nc;
+            pmm *= -(2.0 * m - 1.0) * st;
           }
-          if (m <= CAP) {
-            const double dm = (double)m;
-            const int d0 = m * (m + 1) / 2 + m;
-            double nv = s_norm[d0] * pmm;
-            yj[d0] = make_double2(nv * ec, nv * es);
-            if (m + 1 <= CAP) {
-              double p0 = pmm, p1 = ct * (2.0 * dm + 1.0) * pmm;
-              const int d1 = d0 + m + 1;  // (m + 1)(m + 2) / 2 + m
-              nv = s_norm[d1] * p1;
-              yj[d1] = make_double2(nv * ec, nv * es);
-              int dl = d1;
+          double nv = c_ylm_norm[m * (m + 1) / 2 + m] * pmm;
+          yj[m * (m + 1) / 2 + m] = make_double2(nv * ec, nv * es);
+          if (m + 1 <= CAP) {
+            double p0 = pmm, p1 = ct * (2.0 * m + 1.0) * pmm;
+            nv = c_ylm_norm[(m + 1) * (m + 2) / 2 + m] * p1;
+            yj[(m + 1) * (m + 2) / 2 + m] = make_double2(nv * ec, nv * es);
 #pragma unroll
-              for (int l2 = 0; 2 * k + 2 + l2 <= CAP; ++l2) {  // l = m + 2 + l2
-                const int l = m + 2 + l2;
-                dl += l;  // l (l + 1) / 2 + m
-                if (l <= CAP) {
-                  const double p2 = (ct * (2.0 * l - 1.0) * p1 - (l + dm - 1.0) * p0) * c_recip[l2 + 2];
-                  nv = s_norm[dl] * p2;
-                  yj[dl] = make_double2(nv * ec, nv * es);
-                  p0 = p1;
-                  p1 = p2;
-                }
-              }
+            for (int l = m + 2; l <= CAP; ++l) {
+              const double p2 = (ct * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) * c_recip[l - m];
+              nv = c_ylm_norm[l * (l + 1) / 2 + m] * p2;
+              yj[l * (l + 1) / 2 + m] = make_double2(nv * ec, nv * es);
+              p0 = p1;
+              p1 = p2;
             }
           }
         }
@@ -470,16 +446,11 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
     }
 #pragma unroll
     for (int t = 0; t < TPL; ++t) {
-      if (tq[t] >= 0) {
-        const int4 q = __ldg(tri + lane + 32 * t);
-        const int cpos = col_of ? col_of[q.w] : q.w;
-        if (cpos >= 0) out[s * out_stride + cpos] = acc[t];
-        if (q.z > 0) {  // A[n, l, -m] = (-1)^m conj(A[n, l, m])
-          const int lab_m = q.w - 2 * q.z;
-          const int cm = col_of ? col_of[lab_m] : lab_m;
-          const double sg = (q.z & 1) ? -1.0 : 1.0;
-          if (cm >= 0) out[s * out_stride + cm] = make_double2(sg * acc[t].x, -sg * acc[t].y);
-        }
+      if (cpos[t] >= 0) out[s * out_stride + cpos[t]] = acc[t];
+      const int cm = cneg[t] & 0x3FFFFFFF;
+      if (cneg[t] >= 0 && cm != 0x3FFFFFFF) {  // A[n, l, -m] = (-1)^m conj(A[n, l, m])
+        const double sg = (cneg[t] >> 30) & 1 ? -1.0 : 1.0;
+        out[s * out_stride + cm] = make_double2(sg * acc[t].x, -sg * acc[t].y);
       }
     }
   }

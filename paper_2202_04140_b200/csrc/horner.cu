@@ -474,24 +474,24 @@ __device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<T
     if constexpr (NU >= 4) children<3, NU>(st, (uint32_t)r0.w, H, sd, lane);
   }
   const C4<T> sa = sd.get((uint32_t)r0.z, fl & 3u);
-  if (fl & 16u) {  // order-1 coefficient: c Re(s_a)
+  // an order-1 coefficient (single) has no children, so H = (c, 0), and
+  // s_b = 1 makes the common epilogue c Re(s_a) exactly: one path, no merge
+  C4<T> sb;
+  if (fl & 16u) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if constexpr (sizeof(T) == 8) acc[k] = __fma_rn(c, sa.v[k].x, acc[k]);
-      else acc[k] += (double)(c * sa.v[k].x);
-    }
+    for (int k = 0; k < 4; ++k) sb.v[k] = mk2(T(1), T(0));
   } else {
-    const C4<T> sb = sd.get((uint32_t)r1.z, (fl >> 2) & 3u);
+    sb = sd.get((uint32_t)r1.z, (fl >> 2) & 3u);
+  }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const T abx = fmaT(sa.v[k].x, sb.v[k].x, -mulT(sa.v[k].y, sb.v[k].y));
-      const T aby = fmaT(sa.v[k].x, sb.v[k].y, mulT(sa.v[k].y, sb.v[k].x));
-      if constexpr (sizeof(T) == 8) {
-        acc[k] = __fma_rn(abx, H.v[k].x, acc[k]);
-        acc[k] = __fma_rn(-aby, H.v[k].y, acc[k]);
-      } else {  // the site's sum over roots in fp64
-        acc[k] += (double)fmaT(abx, H.v[k].x, -mulT(aby, H.v[k].y));
-      }
+  for (int k = 0; k < 4; ++k) {
+    const T abx = fmaT(sa.v[k].x, sb.v[k].x, -mulT(sa.v[k].y, sb.v[k].y));
+    const T aby = fmaT(sa.v[k].x, sb.v[k].y, mulT(sa.v[k].y, sb.v[k].x));
+    if constexpr (sizeof(T) == 8) {
+      acc[k] = __fma_rn(abx, H.v[k].x, acc[k]);
+      acc[k] = __fma_rn(-aby, H.v[k].y, acc[k]);
+    } else {  // the site's sum over roots in fp64
+      acc[k] += (double)fmaT(abx, H.v[k].x, -mulT(aby, H.v[k].y));
     }
   }
 }

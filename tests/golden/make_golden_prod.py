@@ -6,7 +6,7 @@ where that tree is mounted; the outputs are committed).  Inputs are NOT
 stored: each is regenerated bit-for-bit from its NumPy seed by the GPU tests
 (tests/_helpers.py seeded_A / seeded_shells), so the fixtures stay small.
 
-    python tests/golden/make_golden_prod.py [cfg2] [cfg3] [cfg4] [cfg5]
+    python tests/golden/make_golden_prod.py [cfg1] [cfg2] [cfg3] [cfg4] [cfg5]
 
 For each config the reference builds the graph (build_graph, graphbuild.py:
 243-268; SHA-256 of serialize_graph recorded), pools (pool/one_particle,
@@ -45,6 +45,7 @@ R_IN, R_CUT = 0.8, 5.0
 
 # config: (D, nu, input, S on the GPU, check sites, J, n_out, input seed, coefficient seed)
 PROD = {
+    "cfg1": dict(D=8, nu=3, input="A", S=1_000, n_check=1000, J=0, n_out=1, seed=101, cseed=102),
     "cfg2": dict(D=12, nu=4, input="A", S=100_000, n_check=2000, J=0, n_out=1, seed=201, cseed=202),
     "cfg3": dict(D=12, nu=4, input="positions", S=20_000, n_check=1000, J=30, n_out=1, seed=301, cseed=302),
     "cfg4": dict(D=16, nu=6, input="A", S=19_000, n_check=24, J=0, n_out=1, seed=401, cseed=402),

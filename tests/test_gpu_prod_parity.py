@@ -96,3 +96,15 @@ def test_cfg5_bench_shape_pool_and_k2_mma(cuda, golden):
     got = plan.evaluate_positions(torch.from_numpy(xyz_np).to(cuda)).cpu().numpy()
     assert got.shape == (S, n_out)
     _gate(got[idx], d)
+
+
+def test_cfg1_every_site(cuda, golden):
+    """BASELINE configs[0]: all 1,000 sites against the reference, recursive
+    and naive (cfg1 all sites)."""
+    d, g, plan = _setup(golden, "cfg1")
+    S, idx = int(d["S"]), d["sites"]
+    assert len(idx) == S == 1000
+    A = torch.from_numpy(seeded_A(S, g.num_seeds, int(d["seed"]))).to(cuda)
+    _gate(plan.evaluate(A).cpu().numpy()[idx], d)
+    _gate(plan.evaluate(A, method="naive").cpu().numpy()[idx], d)
+    _gate(plan.evaluate(A.to(torch.complex64)).cpu().numpy()[idx], d, tol=1e-5)

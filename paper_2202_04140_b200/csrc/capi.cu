@@ -1335,8 +1335,24 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
   // v4 (compile-time degree cap, warp per site) for caps 12 and 14 when the
   // triples fit its accumulators; ACEDAG_POOL=2 forces v2 (CTA per site)
   static const bool force_v2 = getenv("ACEDAG_POOL") && atoi(getenv("ACEDAG_POOL")) == 2;
+  static const bool force_v4 = getenv("ACEDAG_POOL") && atoi(getenv("ACEDAG_POOL")) == 4;
   bool done = false;
-  if (!force_v2 && (cap == 12 || cap == 14) && ntri <= 32 * 16) {
+  // v5 (accumulation on DMMA) for plan-driven pools with pruned tables
+  if (!force_v2 && !force_v4 && prune && (cap == 12 || cap == 14)) {
+    auto launch5 = [&](auto k, int W, size_t sm5) -> cudaError_t {
+      cudaError_t e5 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm5);
+      if (e5 != cudaSuccess) return e5;
+      const int g5 = (int)std::min<int64_t>((S + W - 1) / W, (int64_t)sms * 16);
+      k<<<g5, W * 32, sm5, st>>>(xyz, counts, S, J, r_in, r_cut, col_of, stride, out);
+      return cudaGetLastError();
+    };
+    cudaError_t e5 = cap == 12 ? launch5(dev::pool_positions5<12>, dev::Pool5Geom<12>::kW, dev::Pool5Geom<12>::kSmem)
+                               : launch5(dev::pool_positions5<14>, dev::Pool5Geom<14>::kW, dev::Pool5Geom<14>::kSmem);
+    note_launch();
+    if (e5 != cudaSuccess) return cuda_fail(e5, "pool_positions5");
+    done = true;
+  }
+  if (!done && !force_v2 && (cap == 12 || cap == 14) && ntri <= 32 * 16) {
     auto launch4 = [&](auto k, int W, size_t wb) -> cudaError_t {
       const size_t sm4 = (size_t)W * wb;
       cudaError_t e4 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4);

@@ -477,5 +477,179 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
   }
 }
 
+// --------------------------------------------- K1 v5: accumulation on DMMA
+// Per site the pooled basis is a small matrix product,
+//     A[n][(l, m)] = sum_j WR[j][n] * Y[j][(l, m)],
+// so v5 keeps v4's table phase (lane = neighbour, 16 neighbours per pass,
+// pruned pairs l + m <= CAP) and runs the accumulation as
+// mma.sync.m8n8k4.f64 tiles on the FP64 tensor cores: M = the radial index n
+// (two 8-row tiles), N = the (re, im) columns of the pairs, K = the pass's 16
+// neighbours.  Tables are stored j-fastest with a 20-entry j stride, which
+// keeps both the table writes (lane = j) and the fragment loads free of bank
+// conflicts.  Each warp keeps its site's [16 x 104] accumulator tile in
+// registers (52 doubles per lane) across the passes; the lane that holds an
+// (n, pair) element writes A[n, l, m] and A[n, l, -m] = (-1)^m conj(...).
+template <int CAP>
+struct Pool5Geom {
+  static constexpr int kNB = 16;                                     // neighbours per pass (K)
+  static constexpr int kNJ = 20;                                     // j stride of the tables
+  static constexpr int kC1 = CAP + 1;
+  static constexpr int kMT = (kC1 + 7) / 8;                          // 8-row tiles of n
+  static constexpr int kNP = (CAP / 2 + 1) * (CAP + 1 - CAP / 2);    // pairs with l + m <= CAP
+  static constexpr int kNT = (2 * kNP + 7) / 8;                      // 8-column tiles of (re, im)
+  static constexpr int kRows = kNT * 4;                              // pair rows incl. padding
+  static constexpr size_t kWarpBytes = (size_t)kRows * kNJ * 16 + (size_t)kMT * 8 * kNJ * 8;
+  static constexpr int kW = 8;                                       // warps per CTA (255 registers)
+  static constexpr size_t kOutBytes = (size_t)kMT * kNT * 32 * 8;    // per-lane output columns
+  static constexpr size_t kSmem = (size_t)kW * kWarpBytes + kOutBytes;
+  // pair index of (l, m), m-major (m = 0 first): l from m to CAP - m
+  static __host__ __device__ constexpr int pair(int l, int m) { return m * (CAP + 2 - m) + (l - m); }
+};
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// col_of: label -> output column (-1: unused); requires J passes of <= 16
+// neighbours and a plan whose labels all satisfy l + |m| <= CAP
+template <int CAP>
+__global__ void __launch_bounds__(Pool5Geom<CAP>::kW * 32, 1)
+pool_positions5(const double* __restrict__ xyz, const int32_t* __restrict__ counts, int64_t S, int J, double r_in,
+                double r_cut, const int32_t* __restrict__ col_of, int64_t out_stride, double2* __restrict__ out) {
+  using G = Pool5Geom<CAP>;
+  constexpr int NJ = G::kNJ, NB = G::kNB, MT = G::kMT, NT = G::kNT, C1 = G::kC1, W = G::kW;
+  extern __shared__ __align__(16) unsigned char psm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* Y = reinterpret_cast<double2*>(psm + G::kWarpBytes * warp);  // [kRows][NJ]
+  double* WR = reinterpret_cast<double*>(Y + G::kRows * NJ);            // [MT * 8][NJ]
+  int2* ocol = reinterpret_cast<int2*>(psm + G::kWarpBytes * W);        // [MT][NT][32]
+  // output columns of every accumulator element, per lane (same for all sites):
+  // .x = column of (n, l, m), .y = column of (n, l, -m) | sign bit 30 (-1: none)
+  for (int e = threadIdx.x; e < MT * NT * 32; e += blockDim.x) {
+    const int ln = e & 31, nt = (e >> 5) % NT, mt = (e >> 5) / NT;
+    const int n = mt * 8 + (ln >> 2), p = nt * 4 + (ln & 3);
+    int2 oc = make_int2(-1, -1);
+    if (n <= CAP && p < G::kNP) {
+      int m = 0;
+      while (m < CAP / 2 && p >= G::pair(m + 1, m + 1)) ++m;
+      const int l = p - G::pair(m, m) + m;
+      if (l + n <= CAP) {
+        int base = 0;  // labels before n: sum over n' < n of (CAP - n' + 1)^2
+        for (int q = 0; q < n; ++q) base += (CAP - q + 1) * (CAP - q + 1);
+        const int lab = base + l * l + l + m;
+        oc.x = col_of ? col_of[lab] : lab;
+        if (m > 0) {
+          const int cm = col_of ? col_of[lab - 2 * m] : lab - 2 * m;
+          if (cm >= 0) oc.y = cm | (m & 1) << 30;
+        }
+      }
+    }
+    ocol[e] = oc;
+  }
+  __syncthreads();
+  const double inv_span = 1.0 / (r_cut - r_in);
+  for (int64_t s = (int64_t)blockIdx.x * W + warp; s < S; s += (int64_t)gridDim.x * W) {
+    const int nj = counts ? min(max(counts[s], 0), J) : J;
+    double acc[MT][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int j0 = 0; j0 < nj; j0 += NB) {
+      const int nb = min(NB, nj - j0);
+      if (lane < NB) {
+        const int jl = lane;
+        if (jl < nb) {
+          const double* p = xyz + (s * J + j0 + jl) * 3;
+          const double x = p[0], y = p[1], z = p[2];
+          const double rho2 = x * x + y * y;
+          const double r = sqrt(rho2 + z * z);
+          const double w = r < r_cut ? 0.5 * (1.0 + cospi(r / r_cut)) : 0.0;
+          const double u = 2.0 * fmin(1.0, fmax(0.0, (r - r_in) * inv_span)) - 1.0;
+          {
+            double t0 = 1.0, t1 = u;
+            WR[0 * NJ + jl] = w;
+            if (CAP >= 1) WR[1 * NJ + jl] = w * u;
+#pragma unroll
+            for (int n = 2; n <= CAP; ++n) {
+              const double t2 = 2.0 * u * t1 - t0;
+              WR[n * NJ + jl] = w * t2;
+              t0 = t1;
+              t1 = t2;
+            }
+          }
+          const double rho = sqrt(rho2);
+          const double ct = r > 0.0 ? z / r : 1.0, st = r > 0.0 ? rho / r : 0.0;
+          const double cp = rho > 0.0 ? x / rho : 1.0, sp = rho > 0.0 ? y / rho : 0.0;
+          double ec = 1.0, es = 0.0, pmm = 1.0;
+#pragma unroll
+          for (int m = 0; m <= CAP / 2; ++m) {
+            if (m > 0) {
+              const double nc = ec * cp - es * sp;
+              es = ec * sp + es * cp;
+              ec = nc;
+              pmm *= -(2.0 * m - 1.0) * st;
+            }
+            double nv = c_ylm_norm[m * (m + 1) / 2 + m] * pmm;
+            Y[G::pair(m, m) * NJ + jl] = make_double2(nv * ec, nv * es);
+            if (m + 1 <= CAP - m) {
+              double p0 = pmm, p1 = ct * (2.0 * m + 1.0) * pmm;
+              nv = c_ylm_norm[(m + 1) * (m + 2) / 2 + m] * p1;
+              Y[G::pair(m + 1, m) * NJ + jl] = make_double2(nv * ec, nv * es);
+#pragma unroll
+              for (int l = m + 2; l <= CAP - m; ++l) {
+                const double p2 = (ct * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) * c_recip[l - m];
+                nv = c_ylm_norm[l * (l + 1) / 2 + m] * p2;
+                Y[G::pair(l, m) * NJ + jl] = make_double2(nv * ec, nv * es);
+                p0 = p1;
+                p1 = p2;
+              }
+            }
+          }
+        } else {  // K padding of a short pass: zero weights and finite values
+#pragma unroll
+          for (int n = 0; n < MT * 8; ++n) WR[n * NJ + jl] = 0.0;
+          for (int q = 0; q < G::kRows; ++q) Y[q * NJ + jl] = make_double2(0.0, 0.0);
+        }
+      } else if (j0 == 0) {  // rows of n past CAP and pair rows past kNP: zero once per site
+        for (int q = lane - NB; q < (MT * 8 - C1) * NB; q += 32 - NB)
+          WR[(C1 + q / NB) * NJ + q % NB] = 0.0;
+        for (int q = lane - NB; q < (G::kRows - G::kNP) * NB; q += 32 - NB)
+          Y[(G::kNP + q / NB) * NJ + q % NB] = make_double2(0.0, 0.0);
+      }
+      __syncwarp();
+      // the pass as 4 k-steps of 4 neighbours
+#pragma unroll
+      for (int ks = 0; ks < NB / 4; ++ks) {
+        const int jj = ks * 4 + (lane & 3);
+        double a[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) a[mt] = WR[(mt * 8 + (lane >> 2)) * NJ + jj];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int col = nt * 8 + (lane >> 2);
+          const double b = reinterpret_cast<const double*>(Y + (col >> 1) * NJ + jj)[col & 1];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt][nt], a[mt], b);
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int2 oc = ocol[(mt * NT + nt) * 32 + lane];
+        if (oc.x >= 0) out[s * out_stride + oc.x] = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        if (oc.y >= 0) {
+          const double sg = (oc.y >> 30) & 1 ? -1.0 : 1.0;
+          out[s * out_stride + (oc.y & 0x3FFFFFFF)] = make_double2(sg * acc[mt][nt][0], -sg * acc[mt][nt][1]);
+        }
+      }
+  }
+}
+
 }  // namespace dev
 }  // namespace acedag

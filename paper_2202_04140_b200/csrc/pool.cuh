@@ -489,6 +489,8 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
 // conflicts.  Each warp keeps its site's [16 x 104] accumulator tile in
 // registers (52 doubles per lane) across the passes; the lane that holds an
 // (n, pair) element writes A[n, l, m] and A[n, l, -m] = (-1)^m conj(...).
+// (One pass of 32 neighbours -- every lane in the table phase, 6 warps --
+// ran cfg3 at 32.8 vs 30.9 ms per step: it spills.)
 template <int CAP>
 struct Pool5Geom {
   static constexpr int kNB = 16;                                     // neighbours per pass (K)

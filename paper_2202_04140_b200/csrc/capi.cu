@@ -649,6 +649,8 @@ constexpr int kNC = 8;
 // SMs a concurrent kernel of the same call keeps (the host-path seed gather
 // runs next to the persistent K2 grid); per thread so calls stay independent
 thread_local int t_sm_reserve = 0;
+// the eval_impl input is already k2_horner's tile-major table (positions path)
+thread_local bool t_input_tiled = false;
 // phase events of the eval being launched on this thread (acedag_plan_timing)
 thread_local cudaEvent_t* t_tev = nullptr;
 thread_local bool t_main_marked = false;
@@ -835,8 +837,12 @@ bool run_horner(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
                 Launch& lc, cudaStream_t st, cudaError_t& e) {
   constexpr bool f32 = sizeof(V) == 8;
   const acedag_plan::HornerProg& hp = P->hp[f32 ? 1 : 0];
-  if (!tile_seeds<128, V>(P, A, S, L, slot_label, lc.ws, st, e)) return false;
-  if (e != cudaSuccess) return true;
+  const void* table = A;  // already tile-major (the positions path's pool wrote it)
+  if (!t_input_tiled) {
+    if (!tile_seeds<128, V>(P, A, S, L, slot_label, lc.ws, st, e)) return false;
+    if (e != cudaSuccess) return true;
+    table = lc.ws->tiles.p;
+  }
   mark_prep(st);
   const int64_t ntiles = (S + 127) / 128;
   // fewer tiles than SMs: the grid covers program slices of them too
@@ -851,7 +857,7 @@ bool run_horner(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
     e = lc.ws->tail.alloc((size_t)(ntiles - full) * nch * 128);
     if (e != cudaSuccess) return true;
   }
-  e = launch_horner(P->host.max_order, f32, lc.ws->tiles.p, S, P->U, hp.us, hp.ops.p, hp.chunk.p, hp.croots.p, nch,
+  e = launch_horner(P->host.max_order, f32, table, S, P->U, hp.us, hp.ops.p, hp.chunk.p, hp.croots.p, nch,
                     out, lc.ws->part.p, full, parts, lc.ws->tail.p, grid, st);
   note_launch();
   mark_main(st);
@@ -1306,9 +1312,11 @@ int acedag_pool(int group, int cap, const double* coords, const int32_t* counts,
 // tri/ntri: the triples to compute (NULL = all of this cap)
 // prune: every triple has l + m <= cap (the plan's labels), so the Y_lm
 // tables may skip the pairs above that line (pool_positions4 PRUNE)
+// tile_rows > 0 (pool_positions5 only): write K2's tile-major table
 static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts, int64_t S, int J,
                                double r_in, double r_cut, const int32_t* col_of, const int4* tri,
-                               int ntri, int64_t out_stride, double* A_out, cudaStream_t st, bool prune = false) {
+                               int ntri, int64_t out_stride, double* A_out, cudaStream_t st, bool prune = false,
+                               int tile_rows = 0) {
   if (cap < 0 || cap > ACEDAG_YLM_LMAX) return fail(ACEDAG_EUNSUPPORTED, "degree cap outside [0, 40]");
   if (!(r_cut > r_in) || !(r_in >= 0.0)) return fail(ACEDAG_EINVAL, "need 0 <= r_in < r_cut");
   const int dev = current_device();
@@ -1343,7 +1351,7 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
       cudaError_t e5 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm5);
       if (e5 != cudaSuccess) return e5;
       const int g5 = (int)std::min<int64_t>((S + W - 1) / W, (int64_t)sms * 16);
-      k<<<g5, W * 32, sm5, st>>>(xyz, counts, S, J, r_in, r_cut, col_of, stride, out);
+      k<<<g5, W * 32, sm5, st>>>(xyz, counts, S, J, r_in, r_cut, col_of, stride, out, tile_rows);
       return cudaGetLastError();
     };
     cudaError_t e5 = cap == 12 ? launch5(dev::pool_positions5<12>, dev::Pool5Geom<12>::kW, dev::Pool5Geom<12>::kSmem)
@@ -1352,6 +1360,7 @@ static int pool_positions_impl(int cap, const double* xyz, const int32_t* counts
     if (e5 != cudaSuccess) return cuda_fail(e5, "pool_positions5");
     done = true;
   }
+  if (tile_rows > 0 && !done) return fail(ACEDAG_EINVAL, "tile-major pool output needs pool_positions5");
   if (!done && !force_v2 && (cap == 12 || cap == 14) && ntri <= 32 * 16) {
     auto launch4 = [&](auto k, int W, size_t wb) -> cudaError_t {
       const size_t sm4 = (size_t)W * wb;
@@ -1408,14 +1417,24 @@ int acedag_eval_from_positions(acedag_plan* P, const double* xyz, const int32_t*
     return fail(ACEDAG_ENOMEM, "workspace allocation failed");
   const int cap = P->g->spec.int_cap();
   const size_t osz = out_kind == ACEDAG_OUT_COMPLEX ? 16 : 8;
+  // the pool writes k2_horner's tile-major table itself when that is the
+  // kernel and the DMMA pool runs (no k_tile_seeds pass; ACEDAG_POOL_TILED=0
+  // keeps the site-major workspace)
+  static const bool pool_tiled = !(getenv("ACEDAG_POOL_TILED") && atoi(getenv("ACEDAG_POOL_TILED")) == 0);
+  const bool tiled = pool_tiled && P->tri_pruned && (cap == 12 || cap == 14) && !getenv("ACEDAG_POOL") &&
+                     pick(P, ACEDAG_METHOD_RECURSIVE, ACEDAG_PREC_F64, out_kind) == K2::Horner;
+  if (tiled && W->ws_A.alloc((size_t)((std::min<int64_t>(S, chunk) + 127) / 128) * (U + 1) * 128) != cudaSuccess)
+    return fail(ACEDAG_ENOMEM, "workspace allocation failed");
   for (int64_t s0 = 0; s0 < S; s0 += chunk) {
     const int64_t n = std::min(chunk, S - s0);
     int rc = pool_positions_impl(cap, xyz + s0 * J * 3, counts ? counts + s0 : nullptr, n, J, r_in, r_cut,
                                  P->col_of.p, P->tri.p, (int)P->tri.n, U, reinterpret_cast<double*>(W->ws_A.p), st,
-                                 P->tri_pruned);
+                                 P->tri_pruned, tiled ? U + 1 : 0);
     if (rc) return rc;
+    t_input_tiled = tiled;
     rc = eval_impl(P, ACEDAG_METHOD_RECURSIVE, ACEDAG_PREC_F64, out_kind, W->ws_A.p, n, U,
                    P->slot_identity.p, static_cast<char*>(out) + s0 * P->host.n_out * osz, st);
+    t_input_tiled = false;
     if (rc) return rc;
   }
   return ACEDAG_OK;

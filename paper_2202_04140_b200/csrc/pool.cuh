@@ -516,10 +516,15 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 
 // col_of: label -> output column (-1: unused); requires J passes of <= 16
 // neighbours and a plan whose labels all satisfy l + |m| <= CAP
+// tile_rows > 0: write straight into K2's tile-major seed table
+// [S/128][tile_rows][128] (row = output column; row tile_rows - 1 = the
+// constant ONE) instead of the site-major [S][out_stride] workspace, so the
+// positions path needs no k_tile_seeds pass
 template <int CAP>
 __global__ void __launch_bounds__(Pool5Geom<CAP>::kW * 32, 1)
 pool_positions5(const double* __restrict__ xyz, const int32_t* __restrict__ counts, int64_t S, int J, double r_in,
-                double r_cut, const int32_t* __restrict__ col_of, int64_t out_stride, double2* __restrict__ out) {
+                double r_cut, const int32_t* __restrict__ col_of, int64_t out_stride, double2* __restrict__ out,
+                int tile_rows) {
   using G = Pool5Geom<CAP>;
   constexpr int NJ = G::kNJ, NB = G::kNB, MT = G::kMT, NT = G::kNT, C1 = G::kC1, W = G::kW;
   extern __shared__ __align__(16) unsigned char psm[];
@@ -639,15 +644,19 @@ pool_positions5(const double* __restrict__ xyz, const int32_t* __restrict__ coun
       }
       __syncwarp();
     }
+    // site s, column c -> out[o0 + c * ostep]
+    const int64_t o0 = tile_rows > 0 ? (s >> 7) * (int64_t)tile_rows * 128 + (s & 127) : s * out_stride;
+    const int64_t ostep = tile_rows > 0 ? 128 : 1;
+    if (tile_rows > 0 && lane == 0) out[o0 + (int64_t)(tile_rows - 1) * 128] = make_double2(1.0, 0.0);
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int2 oc = ocol[(mt * NT + nt) * 32 + lane];
-        if (oc.x >= 0) out[s * out_stride + oc.x] = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        if (oc.x >= 0) out[o0 + oc.x * ostep] = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
         if (oc.y >= 0) {
           const double sg = (oc.y >> 30) & 1 ? -1.0 : 1.0;
-          out[s * out_stride + (oc.y & 0x3FFFFFFF)] = make_double2(sg * acc[mt][nt][0], -sg * acc[mt][nt][1]);
+          out[o0 + (oc.y & 0x3FFFFFFF) * ostep] = make_double2(sg * acc[mt][nt][0], -sg * acc[mt][nt][1]);
         }
       }
   }

@@ -1,18 +1,21 @@
 // sm_100a kernels of the evaluator.
 //
-//   K1  pool_*          atomic basis A_{s,k} = sum_j phi_k(particle_j)   (evaluator.py:61-90)
-//   K2  k2_*            recursive DAG program, fused c . A reduction      (evaluator.py:93-110,141)
+//   K1  pool_*          atomic basis (pool.cuh)                          (evaluator.py:61-90)
+//   K2  k2_quad         fp64 order 5-6, forward per-node products, 128-site tiles, TMEM hot rows
+//       k2_mma          >= 8 real outputs: the c . A epilogue as DMMA tiles, 32-site tiles
+//       k2_general      complex coefficients / complex output / 2-7 outputs, 32-site tiles
+//       (k2_horner, the fp64 order <= 4 and fp32 kernel, lives in horner.cu)
 //   K3  k3_naive        naive product basis, fused c . A reduction        (evaluator.py:113-121)
+//   --  k_tile_seeds    tile-major seed table for k2_horner / k2_quad
 //   --  k_eval_nodes    every DAG node, bit-exact (no FMA)                (evaluator.py:93-110)
 //   --  k_reduce_sites  deterministic per-output site sum (energy total)
 //
-// Layout: a CTA owns a tile of 32 sites; lane = site.  The pooled seeds the
-// program references are staged ONCE per tile into shared memory as
-// [slot][32 sites] complex (16 B per lane, conflict-free LDS.128); every warp
-// of the CTA then walks its own chunk of the DFS program, with the DAG
-// record stream read warp-uniformly (one broadcast L1 transaction per
-// record) and the parent value of each level held in registers.  Only one
-// secondary seed is fetched from shared memory per product.
+// The 32-site kernels (k2_mma, k2_general, k3_naive): a CTA owns a tile of
+// 32 sites, lane = site; the seeds the program references are staged once per
+// tile into shared memory as [slot][32 sites] (the rest in a per-CTA global
+// cache), and every warp walks its own chunk of the DFS program with the
+// records read warp-uniformly and the parent value of each level in
+// registers.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(512) k_tile_seeds(const V* __restrict__ A, int
 // ------------------------------------- K2 (four sites per lane, TMEM + smem)
 // 128-site tiles: lane l handles sites l, l+32, l+64, l+96 of the tile, so
 // every program record (its load, decode, seed addressing and loop control)
-// serves four sites -- the per-record overhead that bounds k2_tmem2/3 is
+// serves four sites -- the per-record overhead of narrower tiles is
 // amortised twice as far.  Seed rows are 2 KB ([4][32] c128): the 32 hottest
 // in TMEM (16 columns per lane, one x16 load per fetch, replicated per lane
 // quadrant), the next in shared memory, the tail in the per-CTA global
@@ -568,7 +571,7 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
-    // one partial per (chunk, site), summed in chunk order (as k2_tmem3)
+    // one partial per (chunk, site), summed in chunk order (as k2_horner)
     double* dst = whole ? mypart : tailbuf + (size_t)((it - full_tiles) / tail_parts) * nchunk * 128;
     // chunks handed out dynamically (the partials are indexed by chunk, so
     // the result does not depend on which warp ran which chunk)

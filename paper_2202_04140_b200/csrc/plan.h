@@ -28,12 +28,12 @@ struct alignas(16) Op {
   double c;       // first output's real coefficient (0 if the node carries none)
   uint32_t off;   // byte offset of the seed row in the [slot][32 sites] c128 table
   uint16_t nch;   // number of children that follow in DFS preorder
-  uint16_t skip;  // leading children whose seed is TMEM-resident (k2_tmem);
+  uint16_t skip;  // leading children whose seed is TMEM-resident (k2_quad re-encoding);
                   // a root's second record: bit0/bit1 = its two seeds are
 };
 constexpr uint16_t kSingle = 0xFFFF;
 constexpr uint32_t kRowBytes = 32 * 16;  // one slot row: 32 sites x complex128
-constexpr uint32_t kTmemRows = 128;        // hottest slots k2_tmem keeps in TMEM
+constexpr uint32_t kTmemRows = 128;        // default hot-slot count of the host program view
 
 struct PlanHost {
   int max_order = 2;                 // deepest order in the recursive program
@@ -55,7 +55,7 @@ struct PlanHost {
 
 // Throws std::invalid_argument (bad node id) or std::domain_error (non-target;
 // message carries the tuple repr).
-// hot_rows: seed slots below it are TMEM-resident in the k2_tmem kernels;
+// hot_rows: seed slots below it are ordered first among a node's children;
 // each node's children are ordered with those first and counted in `skip`
 void compile_plan(const Graph& g, const int64_t* node_ids, const double* c_re,
                   const double* c_im, int64_t n_coef, int n_out, int warps, PlanHost& out,

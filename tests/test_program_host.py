@@ -12,7 +12,7 @@ from _helpers import phi_gate, seeded_A
 
 
 def simulate(prog, A):
-    """Walk the program exactly as k2_fast does (per chunk, preorder):
+    """Walk the program in the kernels' order (per chunk, preorder):
     a root is two records (two seeds; slot U is the constant ONE), every
     other record multiplies its seed into the parent value."""
     ops, slots = prog["ops"], prog["slot_label"]

@@ -43,7 +43,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
 
     def compile_one(src: str) -> None:
-        cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", _obj(src), os.path.join(CSRC, src)]
+        extra = os.environ.get("ACEDAG_NVCC_EXTRA", "").split()  # experiment builds only
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", "-o", _obj(src), os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

@@ -20,6 +20,14 @@
 // chunk's per-site partial is stored and the tile's partials are summed in
 // chunk order by warps 0-3 at the start of the CTA's next item (double
 // buffer), so a site's value does not depend on the batch, grid or split.
+//
+// Where the time goes (cfg2, tools/mkvariant.sh -DHX_NOFMA / -DHX_NOSEED /
+// -DHX_NOGL timing builds): with the FMAs and the seed fetches both removed
+// the walk alone still takes 1.29 of 2.02 ms; the FMAs add 0.45 ms, the
+// global tail 0.13 ms.  Time follows the instruction count at ~0.55
+// instructions per clock per scheduler (four in-order warps of dependent
+// control code), so the order-4 program sorts each root's children into
+// same-shape runs that are walked by branch-free loops (run1 / run2).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -86,7 +94,11 @@ __device__ __forceinline__ void tmem_ld(uint32_t addr, uint32_t (&r)[8]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(addr));
 }
+#ifdef HX_NOSEED
+__device__ __forceinline__ void tmem_wait_ld() {}
+#else
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+#endif
 __device__ __forceinline__ void tmem_st8(uint32_t addr, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t a4,
                                          uint32_t a5, uint32_t a6, uint32_t a7) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(addr), "r"(a0),
@@ -214,7 +226,14 @@ struct SeedsH {
   const char* gb;  // global tail row 0 of this tile + lane * sizeof(V)
   // z: TMEM address of the row in this warp's lane quadrant (the program
   // copy of the quadrant carries the lane bits; the allocation base is 0)
+#ifdef HX_NOSEED
+  __device__ __forceinline__ void hot(uint32_t z, Tm& t) const {
+#pragma unroll
+    for (int i = 0; i < kC; ++i) t[i] = z + i;
+  }
+#else
   __device__ __forceinline__ void hot(uint32_t z, Tm& t) const { tmem_ld(z, t); }
+#endif
   __device__ __forceinline__ static C4<T> unpack(const Tm& t) {
     C4<T> s;
 #pragma unroll
@@ -228,6 +247,10 @@ struct SeedsH {
   }
   __device__ __forceinline__ C4<T> sm(uint32_t z) const {
     C4<T> s;
+#ifdef HX_NOSEED
+    for (int k = 0; k < 4; ++k) s.v[k] = mk2(T(z), T(k));
+    return s;
+#endif
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if constexpr (sizeof(T) == 8)
@@ -239,6 +262,13 @@ struct SeedsH {
   }
   __device__ __forceinline__ C4<T> gl(uint32_t z) const {
     C4<T> s;
+#ifdef HX_NOSEED
+    for (int k = 0; k < 4; ++k) s.v[k] = mk2(T(z), T(k));
+    return s;
+#endif
+#ifdef HX_NOGL
+    return sm(z & 0x1FFFFu);
+#endif
 #pragma unroll
     for (int k = 0; k < 4; ++k) s.v[k] = __ldg(reinterpret_cast<const V*>(gb + z + k * kQ));
     return s;
@@ -263,6 +293,10 @@ __device__ __forceinline__ void init_h(C4<T>& H, T c) {
 // H += c s
 template <typename T>
 __device__ __forceinline__ void axpy(C4<T>& H, T c, const C4<T>& s) {
+#ifdef HX_NOFMA
+  H.v[0].x = fmaT(c, s.v[0].x + s.v[3].y, H.v[0].x);
+  return;
+#endif
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     H.v[k].x = fmaT(c, s.v[k].x, H.v[k].x);
@@ -272,6 +306,11 @@ __device__ __forceinline__ void axpy(C4<T>& H, T c, const C4<T>& s) {
 // H = c + c_l s (the accumulator's first term folded into its FMAs)
 template <typename T>
 __device__ __forceinline__ void axpy_init(C4<T>& H, T c, T cl, const C4<T>& s) {
+#ifdef HX_NOFMA
+  init_h(H, c);
+  H.v[0].x = fmaT(cl, s.v[0].x + s.v[3].y, c);
+  return;
+#endif
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     H.v[k].x = fmaT(cl, s.v[k].x, c);
@@ -281,6 +320,10 @@ __device__ __forceinline__ void axpy_init(C4<T>& H, T c, T cl, const C4<T>& s) {
 // Hp += s H
 template <typename T>
 __device__ __forceinline__ void cmac(C4<T>& Hp, const C4<T>& s, const C4<T>& H) {
+#ifdef HX_NOFMA
+  Hp.v[0].x = fmaT(s.v[0].x + s.v[3].y, H.v[0].x, Hp.v[0].x);
+  return;
+#endif
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     Hp.v[k].x = fmaT(s.v[k].x, H.v[k].x, Hp.v[k].x);
@@ -377,7 +420,7 @@ __device__ __forceinline__ void leaves(uint32_t q, uint32_t w, T c, int4 l, C4<T
 // s * (c + sum_leaves c_l s_l) to Hp.  The node record and the one after it
 // (its first leaf) are read together; for the commonest shapes (one or two
 // hot leaves) the leaf seeds and a hot node seed share one TMEM round trip.
-template <uint32_t PC, typename T, bool HYB>
+template <uint32_t PC, bool RUNS, typename T, bool HYB>
 __device__ __forceinline__ void parents(RingH& st, uint32_t n, C4<T>& Hp, const SeedsH<T, HYB>& sd, int lane) {
   using SD = SeedsH<T, HYB>;
 #pragma unroll 1
@@ -385,7 +428,7 @@ __device__ __forceinline__ void parents(RingH& st, uint32_t n, C4<T>& Hp, const 
     const int4 r = st.at(0), l = st.at(1);
     const uint32_t w = (uint32_t)r.w;
     C4<T> H, sp;
-    if (w == kOneHot) {
+    if (!RUNS && w == kOneHot) {
       typename SD::Tm tl;
       sd.hot((uint32_t)l.z, tl);
       if constexpr (PC == 0) {
@@ -397,7 +440,7 @@ __device__ __forceinline__ void parents(RingH& st, uint32_t n, C4<T>& Hp, const 
         tmem_wait_ld();
       }
       axpy_init(H, rec_c<T>(r), rec_c<T>(l), SD::unpack(tl));
-    } else if (w == kTwoHot) {
+    } else if (!RUNS && w == kTwoHot) {
       const int4 l2 = st.at(2);
       typename SD::Tm tl, tl2;
       sd.hot((uint32_t)l.z, tl);
@@ -419,6 +462,106 @@ __device__ __forceinline__ void parents(RingH& st, uint32_t n, C4<T>& Hp, const 
     if constexpr (PC != 0) sp = seed_of<PC>(sd, (uint32_t)r.z);
     cmac(Hp, sp, H);
     st.p += 16 + lw_end(w);
+    st.check(lane);
+  }
+}
+
+// ---- shape-sorted runs (order-4 programs) --------------------------------
+// The walk is bound by its own control chain (record load -> compare ->
+// branch -> next address; ~140 cycles per record per warp with the FMAs and
+// seed fetches removed), so the commonest node shapes get loops with no
+// data-dependent branch: the order-3 children of a root are sorted, inside
+// each seed class, into S1 (exactly one leaf, hot), S2 (exactly two leaves,
+// both hot) and the rest; the root's second record carries the six run
+// lengths.  An S1 node is the two records {c, z, .}{c_l, z_l, .}, an S2 node
+// three; up to 32 records (the checked ring window) go between ring checks,
+// and S1 nodes are taken two at a time so that four seed fetches are in
+// flight behind one wait.
+template <uint32_t PC, typename T, bool HYB>
+__device__ __forceinline__ void run1(RingH& st, uint32_t n, C4<T>& Hp, const SeedsH<T, HYB>& sd, int lane) {
+  using SD = SeedsH<T, HYB>;
+#pragma unroll 1
+  while (n) {
+    const uint32_t m = n < 16u ? n : 16u;
+    n -= m;
+    uint32_t q = st.p;
+    const uint32_t qe = q + m * 32u;
+#pragma unroll 1
+    for (; q + 32 < qe; q += 64) {
+      const int4 ra = lds128(q), la = lds128(q + 16), rb = lds128(q + 32), lb = lds128(q + 48);
+      typename SD::Tm tla, tlb;
+      sd.hot((uint32_t)la.z, tla);
+      sd.hot((uint32_t)lb.z, tlb);
+      C4<T> spa, spb, H;
+      if constexpr (PC == 0) {
+        typename SD::Tm tpa, tpb;
+        sd.hot((uint32_t)ra.z, tpa);
+        sd.hot((uint32_t)rb.z, tpb);
+        tmem_wait_ld();
+        spa = SD::unpack(tpa);
+        spb = SD::unpack(tpb);
+      } else {
+        spa = seed_of<PC>(sd, (uint32_t)ra.z);
+        spb = seed_of<PC>(sd, (uint32_t)rb.z);
+        tmem_wait_ld();
+      }
+      axpy_init(H, rec_c<T>(ra), rec_c<T>(la), SD::unpack(tla));
+      cmac(Hp, spa, H);
+      axpy_init(H, rec_c<T>(rb), rec_c<T>(lb), SD::unpack(tlb));
+      cmac(Hp, spb, H);
+    }
+    if (q < qe) {
+      const int4 r = lds128(q), l = lds128(q + 16);
+      typename SD::Tm tl;
+      sd.hot((uint32_t)l.z, tl);
+      C4<T> sp, H;
+      if constexpr (PC == 0) {
+        typename SD::Tm tp;
+        sd.hot((uint32_t)r.z, tp);
+        tmem_wait_ld();
+        sp = SD::unpack(tp);
+      } else {
+        sp = seed_of<PC>(sd, (uint32_t)r.z);
+        tmem_wait_ld();
+      }
+      axpy_init(H, rec_c<T>(r), rec_c<T>(l), SD::unpack(tl));
+      cmac(Hp, sp, H);
+    }
+    st.p = qe;
+    st.check(lane);
+  }
+}
+
+template <uint32_t PC, typename T, bool HYB>
+__device__ __forceinline__ void run2(RingH& st, uint32_t n, C4<T>& Hp, const SeedsH<T, HYB>& sd, int lane) {
+  using SD = SeedsH<T, HYB>;
+#pragma unroll 1
+  while (n) {
+    const uint32_t m = n < 10u ? n : 10u;
+    n -= m;
+    uint32_t q = st.p;
+    const uint32_t qe = q + m * 48u;
+#pragma unroll 1
+    for (; q < qe; q += 48) {
+      const int4 r = lds128(q), l = lds128(q + 16), l2 = lds128(q + 32);
+      typename SD::Tm tl, tl2;
+      sd.hot((uint32_t)l.z, tl);
+      sd.hot((uint32_t)l2.z, tl2);
+      C4<T> sp, H;
+      if constexpr (PC == 0) {
+        typename SD::Tm tp;
+        sd.hot((uint32_t)r.z, tp);
+        tmem_wait_ld();
+        sp = SD::unpack(tp);
+      } else {
+        sp = seed_of<PC>(sd, (uint32_t)r.z);
+        tmem_wait_ld();
+      }
+      axpy_init(H, rec_c<T>(r), rec_c<T>(l), SD::unpack(tl));
+      axpy(H, rec_c<T>(l2), SD::unpack(tl2));
+      cmac(Hp, sp, H);
+    }
+    st.p = qe;
     st.check(lane);
   }
 }
@@ -447,9 +590,9 @@ template <int D, int NU, typename T, bool HYB>
 __device__ __forceinline__ void children(RingH& st, uint32_t w, C4<T>& Hp, const SeedsH<T, HYB>& sd, int lane) {
   const uint32_t nh = w_nhot(w), ns = w_nsm(w), ng = w_nch(w) - nh - ns;
   if constexpr (D == NU - 1) {
-    parents<0>(st, nh, Hp, sd, lane);
-    parents<1>(st, ns, Hp, sd, lane);
-    if (HYB) parents<2>(st, ng, Hp, sd, lane);
+    parents<0, false>(st, nh, Hp, sd, lane);
+    parents<1, false>(st, ns, Hp, sd, lane);
+    if (HYB) parents<2, false>(st, ng, Hp, sd, lane);
   } else if constexpr (D < NU - 1) {
     inner<D, NU, 0>(st, nh, Hp, sd, lane);
     inner<D, NU, 1>(st, ns, Hp, sd, lane);
@@ -462,6 +605,18 @@ __device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<T
   const int4 r0 = st.at(0), r1 = st.at(1);
   const T c = rec_c<T>(r0);
   const uint32_t fl = (uint32_t)r1.w;
+  if (fl & 16u) {
+    // an order-1 coefficient: phi += c Re(s_a), no children
+    const C4<T> sa = sd.get((uint32_t)r0.z, fl & 3u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (sizeof(T) == 8) acc[k] = __fma_rn(sa.v[k].x, c, acc[k]);
+      else acc[k] += (double)mulT(sa.v[k].x, c);
+    }
+    st.p += 32;
+    st.check(lane);
+    return;
+  }
   C4<T> H;
   if constexpr (NU == 3) {
     leaves(st.p + 32, (uint32_t)r0.w, c, st.at(2), H, sd);
@@ -471,18 +626,31 @@ __device__ __forceinline__ void root(RingH& st, double (&acc)[4], const SeedsH<T
     init_h(H, c);
     st.p += 32;
     st.check(lane);
-    if constexpr (NU >= 4) children<3, NU>(st, (uint32_t)r0.w, H, sd, lane);
+    if constexpr (NU == 4) {
+      // run lengths of the class-and-shape-sorted children: r0.w = the general
+      // runs (hot | shared << 10 | global << 20); r1.x / r1.y = S1 | S2 << 16
+      // of the hot / shared classes; r1.w >> 8 = S1 | S2 << 12 of the global one
+      const uint32_t wg = (uint32_t)r0.w, wh = (uint32_t)r1.x, ws = (uint32_t)r1.y;
+      run1<0>(st, wh & 0xFFFFu, H, sd, lane);
+      run2<0>(st, wh >> 16, H, sd, lane);
+      parents<0, true>(st, wg & 1023u, H, sd, lane);
+      if (ws | (wg & 0xFFC00u)) {
+        run1<1>(st, ws & 0xFFFFu, H, sd, lane);
+        run2<1>(st, ws >> 16, H, sd, lane);
+        parents<1, true>(st, (wg >> 10) & 1023u, H, sd, lane);
+      }
+      if (HYB && (fl >> 8 | wg >> 20)) {
+        run1<2>(st, (fl >> 8) & 0xFFFu, H, sd, lane);
+        run2<2>(st, fl >> 20, H, sd, lane);
+        parents<2, true>(st, wg >> 20, H, sd, lane);
+      }
+    } else if constexpr (NU > 4) {
+      children<3, NU>(st, (uint32_t)r0.w, H, sd, lane);
+    }
   }
-  const C4<T> sa = sd.get((uint32_t)r0.z, fl & 3u);
-  // an order-1 coefficient (single) has no children, so H = (c, 0), and
-  // s_b = 1 makes the common epilogue c Re(s_a) exactly: one path, no merge
-  C4<T> sb;
-  if (fl & 16u) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) sb.v[k] = mk2(T(1), T(0));
-  } else {
-    sb = sd.get((uint32_t)r1.z, (fl >> 2) & 3u);
-  }
+  // (a branch-free form -- three predicated load groups into the same
+  // registers -- spilled and ran 2.42 vs 1.96 ms at cfg2)
+  const C4<T> sa = sd.get((uint32_t)r0.z, fl & 3u), sb = sd.get((uint32_t)r1.z, (fl >> 2) & 3u);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const T abx = fmaT(sa.v[k].x, sb.v[k].x, -mulT(sa.v[k].y, sb.v[k].y));
@@ -795,7 +963,7 @@ struct HornerEnc {
     const uint32_t sa = slot(a), sb = slot(b);
     const bool single = sb == U;
     const uint32_t fl = cls(sa) | (single ? 0u : cls(sb)) << 2 | (single ? 16u : 0u);
-    const std::vector<size_t> kids = kids_from(pos + 2, a.nch);  // children follow the pair
+    std::vector<size_t> kids = kids_from(pos + 2, a.nch);  // children follow the pair
     if (nu == 3) {
       size_t bb = 0;
       bool first = true;
@@ -821,8 +989,42 @@ struct HornerEnc {
       cls_rec.push_back((uint8_t)cls(sa));
       cls_rec.push_back((uint8_t)(single ? 0 : cls(sb)));
       uint32_t n = 0, nh = 0, ns = 0;
+      if (nu == 4) {
+        // shape-sorted runs: per class S1 (one hot leaf), S2 (two hot leaves), the rest
+        auto shape = [&](size_t k) -> uint32_t {
+          const std::vector<size_t> lv = kids_of(k);
+          if (lv.empty() || lv.size() > 2) return 2u;
+          for (size_t q : lv)
+            if (cls(slot(H.ops[q])) != 0) return 2u;
+          return (uint32_t)lv.size() - 1u;
+        };
+        std::stable_sort(kids.begin(), kids.end(), [&](size_t a, size_t b) {
+          const uint32_t ca = cls(slot(H.ops[a])), cb = cls(slot(H.ops[b]));
+          return ca != cb ? ca < cb : shape(a) < shape(b);
+        });
+        runs4 = {};
+        for (size_t k : kids) {
+          const uint32_t sh = shape(k);
+          if (sh < 2) runs4.r[cls(slot(H.ops[k]))][sh]++;
+        }
+      }
       for (size_t k : kids) count(cls(slot(H.ops[k])), node(k, 3), n, nh, ns);
       out[me].w = pack(n, nh, ns);
+      if (nu == 4) {
+        // order-4 roots carry run lengths instead (see hdev::root): general
+        // runs in r0.w, S1 / S2 runs in the second record's free fields
+        const uint32_t byc[3] = {nh, ns, n - nh - ns};
+        uint32_t gen[3];
+        for (int c = 0; c < 3; ++c) {
+          gen[c] = byc[c] - runs4.r[c][0] - runs4.r[c][1];
+          if (gen[c] > 1023u || runs4.r[c][0] > 4095u || runs4.r[c][1] > 4095u) ok = false;
+        }
+        out[me].w = gen[0] | gen[1] << 10 | gen[2] << 20;
+        out[me + 1].w |= runs4.r[2][0] << 8 | runs4.r[2][1] << 20;
+        const uint64_t bits = (uint64_t)(runs4.r[0][0] | runs4.r[0][1] << 16) |
+                              (uint64_t)(runs4.r[1][0] | runs4.r[1][1] << 16) << 32;
+        run_bits.emplace_back(me + 1, bits);
+      }
       nroots++;
     }
     size_t q = pos + 2;
@@ -830,6 +1032,10 @@ struct HornerEnc {
     return q;
   }
   int32_t nroots = 0;
+  struct Runs4 { uint32_t r[3][2]; } runs4{};
+  // (record index, packed run lengths) of the roots' second records (order 4):
+  // written into the coefficient field after the fp32 coefficient conversion
+  std::vector<std::pair<size_t, uint64_t>> run_bits;
 };
 }  // namespace
 
@@ -899,6 +1105,7 @@ bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::
       const uint64_t u = b;
       std::memcpy(&o.c, &u, 8);
     }
+  for (const auto& rb : E.run_bits) std::memcpy(&out[rb.first].c, &rb.second, 8);
   out.resize(4 * n);
   for (size_t q = 1; q < 4; ++q)
     for (size_t i = 0; i < n; ++i) {
@@ -935,6 +1142,11 @@ cudaError_t launch_horner(int nu, bool f32, const void* Tab, int64_t S, int U, i
                                      grid, st)                                                                \
              : launch_nu<N, T, false>(Tab, S, U, us, ops, chunk, croots, nchunk, out, part, full, parts, tail, \
                                       grid, st)
+#ifdef ACEDAG_HORNER_FAST  // experiment builds: order 4 only (tools/mkvariant.sh)
+  if (nu != 4) return cudaErrorInvalidValue;
+  if (f32) { ACEDAG_H(4, float); }
+  ACEDAG_H(4, double);
+#else
   if (f32) {
     switch (nu) {
       case 2: ACEDAG_H(2, float);
@@ -953,6 +1165,7 @@ cudaError_t launch_horner(int nu, bool f32, const void* Tab, int64_t S, int U, i
     case 6: ACEDAG_H(6, double);
     default: return cudaErrorInvalidValue;
   }
+#endif
 #undef ACEDAG_H
 }
 

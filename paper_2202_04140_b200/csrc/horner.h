@@ -26,6 +26,12 @@ namespace acedag {
 // global row -> byte row*2048 (c128) or row*1024 (c64)).  w: nch | nhot << 15
 // | nsm << 22 (children by class, in that order).  A root is two records; the second carries w = cls_a | cls_b << 2 |
 // single << 4 (single: an order-1 coefficient, phi += c Re(s_a)).
+// Order-4 programs (round 2): a root's order-3 children are sorted, inside
+// each seed class, into S1 (one leaf, hot), S2 (two leaves, both hot) and the
+// rest, and the root carries the run lengths instead of the class counts:
+// r0.w = general runs (hot | shared << 10 | global << 20); second record:
+// c bits = S1 | S2 << 16 of the hot (low word) and shared (high word)
+// classes, w |= S1 << 8 | S2 << 20 of the global class.
 struct alignas(16) OpH {
   double c;
   uint32_t z;

@@ -107,10 +107,6 @@ def simulate_horner(h, A):
         assert (cls == 1 and s < hot + us) or (cls == 2 and s >= hot + us)
         return seeds[:, s]
 
-    def cls_of(j, w):  # inner record: counts nch | nhot << 15 | nsm << 22
-        nh, ns = (w >> 15) & 127, w >> 22
-        return 0 if j < nh else (1 if j < nh + ns else 2)
-
     def leaf_cls(j, w):  # last inner order: byte ends hot | shared << 10 | all << 20
         return 0 if 16 * j < (w & 1023) else (1 if 16 * j < ((w >> 10) & 1023) else 2)
 
@@ -127,15 +123,32 @@ def simulate_horner(h, A):
             H = H + r["c"] * seed(r["z"], leaf_cls(j, w))
         return H
 
-    def children(w, D, Hp):
+    def children(w, D, Hp, counts=None):
         nonlocal pos
-        for j in range(w & 0x7FFF):
-            r = ops[pos]
-            pos += 1
-            H = np.full(A.shape[0], r["c"], complex)
-            H = leaves(r["w"], H) if D == nu - 1 else children(r["w"], D + 1, H)
-            Hp = Hp + seed(r["z"], cls_of(j, w)) * H
+        if counts is None:  # inner record: nch | nhot << 15 | nsm << 22
+            nh, ns = (w >> 15) & 127, w >> 22
+            counts = (nh, ns, (w & 0x7FFF) - nh - ns)
+        for c, n in enumerate(counts):
+            for _ in range(n):
+                r = ops[pos]
+                pos += 1
+                H = np.full(A.shape[0], r["c"], complex)
+                H = leaves(r["w"], H) if D == nu - 1 else children(r["w"], D + 1, H)
+                Hp = Hp + seed(r["z"], c) * H
         return Hp
+
+    def root4_counts(r0, r1):
+        """Order-4 roots: the children are sorted by seed class and, inside a
+        class, into S1 (one hot leaf), S2 (two hot leaves) and general runs;
+        r0.w = general runs (10 bits per class), r1.c bits = S1 | S2 << 16 of
+        the hot (low word) / shared (high word) classes, r1.w >> 8 = S1 | S2 << 12
+        of the global class.  Returns (per-class totals, S1/S2 runs)."""
+        wg, fl = int(r0["w"]), int(r1["w"])
+        bits = int(np.array([r1["c"]], "<f8").view("<u8")[0])
+        wh, ws = bits & 0xFFFFFFFF, bits >> 32
+        runs = [(wh & 0xFFFF, wh >> 16), (ws & 0xFFFF, ws >> 16), ((fl >> 8) & 0xFFF, fl >> 20)]
+        gen = [wg & 1023, (wg >> 10) & 1023, wg >> 20]
+        return tuple(a + b + g for (a, b), g in zip(runs, gen)), runs
 
     phi = np.zeros(A.shape[0])
     chunk, croots = h["chunk"], h["croots"]
@@ -148,7 +161,22 @@ def simulate_horner(h, A):
             H = np.full(A.shape[0], r0["c"], complex)
             if nu == 3:
                 H = leaves(int(r0["w"]), H)
-            elif nu >= 4:
+            elif nu == 4 and not fl & 16:
+                counts, runs = root4_counts(r0, r1)
+                p0 = pos
+                H = children(0, 3, H, counts)
+                # the S1 / S2 runs really are one- / two-hot-leaf nodes, in that order per class
+                q = p0
+                for c, n in enumerate(counts):
+                    for j in range(n):
+                        w = int(ops[q]["w"])
+                        if j < runs[c][0]:
+                            assert w == (16 | 16 << 10 | 16 << 20)
+                        elif j < runs[c][0] + runs[c][1]:
+                            assert w == (32 | 32 << 10 | 32 << 20)
+                        q += 1 + (w >> 20) // 16
+                assert q == pos
+            elif nu > 4:
                 H = children(int(r0["w"]), 3, H)
             sa = seed(r0["z"], fl & 3)
             phi = phi + (r0["c"] * sa.real if fl & 16 else (sa * seed(r1["z"], (fl >> 2) & 3) * H).real)

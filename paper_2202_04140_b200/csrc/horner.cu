@@ -273,15 +273,36 @@ struct SeedsH {
     for (int k = 0; k < 4; ++k) s.v[k] = __ldg(reinterpret_cast<const V*>(gb + z + k * kQ));
     return s;
   }
+  // a seed of any class (roots): every path loads into the same raw words,
+  // so the paths merge without register copies (cfg2 K2 1.959 -> 1.941 ms,
+  // fp32 1.331 -> 1.298)
   __device__ __forceinline__ C4<T> get(uint32_t z, uint32_t cls) const {
+    Tm t;
     if (cls == 0) {
-      Tm t;
       hot(z, t);
       tmem_wait_ld();
-      return unpack(t);
+    } else if (!HYB || cls == 1) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if constexpr (sizeof(T) == 8)
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n"
+                       : "=r"(t[4 * k]), "=r"(t[4 * k + 1]), "=r"(t[4 * k + 2]), "=r"(t[4 * k + 3])
+                       : "r"(sb + z + k * kQ));
+        else
+          asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(t[2 * k]), "=r"(t[2 * k + 1]) : "r"(sb + z + k * kQ));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if constexpr (sizeof(T) == 8)
+          asm volatile("ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];\n"
+                       : "=r"(t[4 * k]), "=r"(t[4 * k + 1]), "=r"(t[4 * k + 2]), "=r"(t[4 * k + 3])
+                       : "l"(gb + z + k * kQ));
+        else
+          asm volatile("ld.global.nc.v2.b32 {%0, %1}, [%2];\n" : "=r"(t[2 * k]), "=r"(t[2 * k + 1]) : "l"(gb + z + k * kQ));
+      }
     }
-    if (!HYB || cls == 1) return sm(z);
-    return gl(z);
+    return unpack(t);
   }
 };
 

@@ -180,6 +180,10 @@ struct Stream {
 };
 
 __device__ __forceinline__ double rec_c(int4 r) { return __hiloint2double(r.y, r.x); }
+// A warp-uniform value, declared so to the compiler (REDUX.OR into a uniform
+// register): the program walk's control words are the same in every lane,
+// and branches on them then carry no divergence bookkeeping (see horner.cu).
+__device__ __forceinline__ uint32_t uni(uint32_t v) { return __reduce_or_sync(0xffffffffu, v); }
 __device__ __forceinline__ uint32_t rec_off(int4 r) { return (uint32_t)r.z; }
 __device__ __forceinline__ uint32_t rec_nch(int4 r) { return (uint32_t)r.w & 0xFFFFu; }
 
@@ -431,7 +435,8 @@ __device__ __forceinline__ void k2q_visit(Ring3& st, uint32_t n, uint32_t nh, co
       const double c = rec_c(r);
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[k] = __fma_rn(c, v.v[k].x, acc[k]);
-      k2q_visit<D + 1, NU, MAXU, HYB>(st, rec_nch(r), (uint32_t)r.w >> 16, v, acc, sd, lane);
+      const uint32_t w = uni((uint32_t)r.w);
+      k2q_visit<D + 1, NU, MAXU, HYB>(st, w & 0xFFFFu, w >> 16, v, acc, sd, lane);
     }
   }
 }
@@ -445,7 +450,7 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
         double* __restrict__ out, double2* __restrict__ gcache, double* __restrict__ part, int64_t full_tiles,
         int tail_parts, double* __restrict__ tailbuf) {
   unsigned char* smem = g_smem;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (int)uni(threadIdx.x >> 5);
   const int rows = U + 1;
   const int hot = rows < (int)kTmemRowsQ ? rows : (int)kTmemRowsQ;
   const int cold = rows - hot;
@@ -484,7 +489,8 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
     const int64_t tile = whole ? it : full_tiles + (it - full_tiles) / tail_parts;
     const int slice = whole ? 0 : (int)((it - full_tiles) % tail_parts);
     const int nsl = whole ? 1 : tail_parts;
-    const int cb = (int)((int64_t)slice * nchunk / nsl), ce = (int)((int64_t)(slice + 1) * nchunk / nsl);
+    const int cb = (int)uni((uint32_t)((int64_t)slice * nchunk / nsl)),
+              ce = (int)uni((uint32_t)((int64_t)(slice + 1) * nchunk / nsl));
     const double2* row[4];
     bool ok[4];
 #pragma unroll
@@ -577,23 +583,23 @@ k2_quad(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restr
     // the result does not depend on which warp ran which chunk)
     for (int ci = cb + warp; ci < ce;) {
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
-      st.begin(reinterpret_cast<const int4*>(ops) + b, (uint32_t)(e - b), ring, lane);
+      st.begin(reinterpret_cast<const int4*>(ops) + b, uni((uint32_t)(e - b)), ring, lane);
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       while (st.i < st.n) {
         const int4 r0 = st.at(0), r1 = st.at(1);
         st.advance(2, lane);
-        const uint32_t fl = (uint32_t)r1.w >> 16;
+        const uint32_t fl = uni((uint32_t)r1.w) >> 16, w0 = uni((uint32_t)r0.w);
         const C4 v = cmul4(sd.get((uint32_t)r0.z, fl & 1u), sd.get((uint32_t)r1.z, (fl >> 1) & 1u));
         const double c = rec_c(r0);
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[k] = __fma_rn(c, v.v[k].x, acc[k]);
-        k2q_visit<3, NU, MAXU, HYB>(st, rec_nch(r0), (uint32_t)r0.w >> 16, v, acc, sd, lane);
+        k2q_visit<3, NU, MAXU, HYB>(st, w0 & 0xFFFFu, w0 >> 16, v, acc, sd, lane);
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) dst[(size_t)ci * 128 + k * 32 + lane] = acc[k];
       int nx = 0;
       if (lane == 0) nx = atomicAdd(dyn, 1);
-      ci = __shfl_sync(0xffffffffu, nx, 0);
+      ci = (int)uni((uint32_t)nx);  // lane 0's value (the others hold 0)
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -746,7 +752,7 @@ __device__ __forceinline__ void k2mma_visit(Stream& st, uint32_t n, double2 pv, 
       const double2 v = cmul(sd(rec_off(r)), pv);
       sk.store(v.x);
       sk.flush_ready();
-      k2mma_visit<D + 1, NU, HYB>(st, rec_nch(r), v, sk, sd);
+      k2mma_visit<D + 1, NU, HYB>(st, uni((uint32_t)r.w) & 0xFFFFu, v, sk, sd);
     }
   }
 }
@@ -762,7 +768,7 @@ k2_mma(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restri
   double2* sA = reinterpret_cast<double2*>(smem);
   const uint32_t rings = (uint32_t)((size_t)Us * 32 * sizeof(double2));
   const uint32_t stgs = rings + WARPS * 64 * 16;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (int)uni(threadIdx.x >> 5);
   double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
   Seeds<double, HYB> sd;
   sd.s = (uint32_t)(lane * 16);
@@ -789,7 +795,7 @@ k2_mma(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restri
       for (int n = 0; n < MmaSink::kNT; ++n) sk.acc[m][n][0] = sk.acc[m][n][1] = 0.0;
     for (int ci = warp; ci < nchunk; ci += WARPS) {
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
-      st.begin(prog + b, (uint32_t)(e - b), rings + warp * 64 * 16, lane);
+      st.begin(prog + b, uni((uint32_t)(e - b)), rings + warp * 64 * 16, lane);
       sk.begin(b);
       while (st.i < st.n) {
         const int4 r0 = st.at(0), r1 = st.at(1);
@@ -798,7 +804,7 @@ k2_mma(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __restri
         sk.store(v.x);
         sk.store(0.0);  // the root's second record carries no coefficients
         sk.flush_ready();
-        k2mma_visit<3, NU, HYB>(st, rec_nch(r0), v, sk, sd);
+        k2mma_visit<3, NU, HYB>(st, uni((uint32_t)r0.w) & 0xFFFFu, v, sk, sd);
       }
       sk.finish();
     }

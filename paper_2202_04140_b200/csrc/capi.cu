@@ -611,7 +611,7 @@ int acedag_plan_program_horner(const acedag_graph* h, const int64_t* node_ids, c
   std::vector<int32_t> ch, cr;
   try {
     compile_plan(h->g, node_ids, c_re, nullptr, n_coef, 1, warps, H, (uint32_t)hot);
-    if (!encode_horner(H, false, (uint32_t)hot, (uint32_t)us, out, ch, cr))
+    if (!encode_horner(H, false, (uint32_t)hot, (uint32_t)us, out, ch, cr, true))
       return fail(ACEDAG_EUNSUPPORTED, "program does not fit the k2_horner record fields");
   } catch (const std::domain_error& e) {
     return fail(ACEDAG_ENOTTARGET, e.what());

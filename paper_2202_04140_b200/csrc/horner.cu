@@ -222,6 +222,13 @@ struct RingH {
 };
 
 // ------------------------------------------------------------------- seeds
+// programs come in four copies (one per TMEM lane quadrant, the lane bits
+// folded into the hot offsets) except the deep fp32 ones: at order 5-6 the
+// copies (cfg4: 59 MB each against 126 MB of L2) stream from HBM, and one copy
+// with the quadrant bits added per fetch runs cfg4 fp32 at 453 vs 389 k
+// sites/s (fp64 at order 5-6 spills and is not the default there)
+__host__ __device__ constexpr bool quad_copies(int nu, bool f32) { return nu <= 4 || !f32; }
+
 template <typename T, bool HYB>
 struct SeedsH {
   using V = typename HTr<T>::V;
@@ -229,6 +236,7 @@ struct SeedsH {
   static constexpr uint32_t kQ = HTr<T>::kRow / 4;  // bytes between a lane's four sites in a row
   using Tm = uint32_t[kC];
   uint32_t tq;     // TMEM address of this warp's lane quadrant, column 0
+  uint32_t tqo;    // added to every hot offset: 0 with per-quadrant program copies, else the lane bits
   uint32_t sb;     // shared address of cold row 0 + lane * sizeof(V)
   const char* gb;  // global tail row 0 of this tile + lane * sizeof(V)
   // z: TMEM address of the row in this warp's lane quadrant (the program
@@ -239,7 +247,7 @@ struct SeedsH {
     for (int i = 0; i < kC; ++i) t[i] = z + i;
   }
 #else
-  __device__ __forceinline__ void hot(uint32_t z, Tm& t) const { tmem_ld(z, t); }
+  __device__ __forceinline__ void hot(uint32_t z, Tm& t) const { tmem_ld(z + tqo, t); }
 #endif
   __device__ __forceinline__ static C4<T> unpack(const Tm& t) {
     C4<T> s;
@@ -730,6 +738,7 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
   if (tbase != 0) __trap();  // the program's TMEM addresses assume the whole TMEM at column 0
   SeedsH<T, HYB> sd;
   sd.tq = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+  sd.tqo = quad_copies(NU, sizeof(T) == 4) ? 0u : sd.tq;
   sd.sb = sbase + (uint32_t)(lane * sizeof(V));
   sd.gb = nullptr;
   const uint32_t ring = rings + (uint32_t)warp * kHornerRing;
@@ -816,7 +825,8 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
     for (int ci = cb + warp; ci < ce;) {
       const int32_t b = __ldg(chunk + ci), e = __ldg(chunk + ci + 1);
       const int32_t nr = (int32_t)uni((uint32_t)__ldg(croots + ci));
-      st.begin(reinterpret_cast<const int4*>(ops) + (size_t)(warp & 3) * nops + b, (uint32_t)(e - b), ring, lane);
+      st.begin(reinterpret_cast<const int4*>(ops) + (quad_copies(NU, sizeof(T) == 4) ? (size_t)(warp & 3) * nops : (size_t)0) + b,
+               (uint32_t)(e - b), ring, lane);
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       for (int32_t k = 0; k < nr; ++k) root<NU>(st, acc, sd, lane);
 #pragma unroll
@@ -1070,7 +1080,7 @@ struct HornerEnc {
 }  // namespace
 
 bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::vector<OpH>& out,
-                   std::vector<int32_t>& chunk, std::vector<int32_t>& croots) {
+                   std::vector<int32_t>& chunk, std::vector<int32_t>& croots, bool four_copies) {
   out.clear();
   const size_t nchunk = H.chunk.size() > 0 ? H.chunk.size() - 1 : 0;
   HornerEnc E{H, hot, us, (uint32_t)H.slot_label.size(), H.max_order, out, f32 ? 8u : 16u,
@@ -1136,6 +1146,7 @@ bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::
       std::memcpy(&o.c, &u, 8);
     }
   for (const auto& rb : E.run_bits) std::memcpy(&out[rb.first].c, &rb.second, 8);
+  if (!four_copies && !hdev::quad_copies(H.max_order, f32)) return E.ok && n < (size_t)INT32_MAX;
   out.resize(4 * n);
   for (size_t q = 1; q < 4; ++q)
     for (size_t i = 0; i < n; ++i) {

@@ -54,8 +54,10 @@ constexpr uint32_t kMaxLeaves = 30;
 // out holds four copies of the program (one per TMEM lane quadrant: hot
 // records' z carries the quadrant's lane bits), chunk offsets index copy 0.
 // Returns false when a count does not fit its field (another kernel is used).
+// Programs deeper than order 4 are emitted once (the kernel adds the quadrant
+// bits per fetch) unless four_copies asks for the four-copy view (host inspection).
 bool encode_horner(const PlanHost& H, bool f32, uint32_t hot, uint32_t us, std::vector<OpH>& out,
-                   std::vector<int32_t>& chunk, std::vector<int32_t>& croots);
+                   std::vector<int32_t>& chunk, std::vector<int32_t>& croots, bool four_copies = false);
 
 // shared-memory rows k2_horner can hold besides its rings
 int horner_us_max(size_t smem_optin, bool f32, int nu);

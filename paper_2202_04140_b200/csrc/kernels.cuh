@@ -896,7 +896,7 @@ __device__ __forceinline__ const Op* k2g_visit(const Op* p, const Op* base, uint
       OpR r = load_op(p);
       const double2 v = cmul(sd(r.off), pv);
       acc_general<NC>(acc, v, p - base, cre, cim, n_out, o0, nc);
-      p = k2g_visit<D + 1, NU, NC, HYB>(p + 1, base, r.nch, v, acc, sd, cre, cim, n_out, o0, nc);
+      p = k2g_visit<D + 1, NU, NC, HYB>(p + 1, base, uni(r.nch), v, acc, sd, cre, cim, n_out, o0, nc);
     }
     return p;
   }
@@ -911,7 +911,7 @@ k2_general(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __re
   unsigned char* smem = g_smem;
   double2* sA = reinterpret_cast<double2*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)Us * 32 * sizeof(double2));
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (int)uni(threadIdx.x >> 5), W = blockDim.x >> 5;
   double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
   Seeds<double, HYB> sd;
   sd.s = (uint32_t)(lane * 16);
@@ -933,7 +933,7 @@ k2_general(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __re
         OpR r0 = load_op(p), r1 = load_op(p + 1);
         const double2 v = cmul(sd(r0.off), sd(r1.off));
         acc_general<NC>(acc, v, p - ops, cre, cim, n_out, o0, nc);
-        p = k2g_visit<3, NU, NC, HYB>(p + 2, ops, r0.nch, v, acc, sd, cre, cim, n_out, o0, nc);
+        p = k2g_visit<3, NU, NC, HYB>(p + 2, ops, uni(r0.nch), v, acc, sd, cre, cim, n_out, o0, nc);
       }
     }
     // reduce over warps, one output at a time, fixed order
@@ -969,7 +969,7 @@ k3_naive(const double2* __restrict__ A, int64_t S, int L, const uint16_t* __rest
   unsigned char* smem = g_smem;
   double2* sA = reinterpret_cast<double2*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)Us * 32 * sizeof(double2));
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (int)uni(threadIdx.x >> 5), W = blockDim.x >> 5;
   double2* gA = HYB ? gcache + (size_t)blockIdx.x * (U + 1 - Us) * 32 : nullptr;
   SlotTab<HYB> tab{sA, gA, (uint32_t)Us, lane};
   const int64_t ntiles = (S + 31) / 32;

@@ -364,7 +364,7 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
   using G = Pool4Geom<CAP, PRUNE>;
   constexpr int C1 = G::kC1, NPp = G::kNPp, W = G::kW, NB = G::kNB;
   extern __shared__ __align__(16) unsigned char psm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (int)uni(threadIdx.x >> 5);  // warp-uniform, told to the compiler
   double2* Y = reinterpret_cast<double2*>(psm + G::kWarpBytes * warp);  // [NB][NPp]
   double* WR = reinterpret_cast<double*>(Y + NB * NPp);                 // [NB][C1]
   const double inv_span = 1.0 / (r_cut - r_in);
@@ -386,7 +386,7 @@ pool_positions4(const double* __restrict__ xyz, const int32_t* __restrict__ coun
     }
   }
   for (int64_t s = (int64_t)blockIdx.x * W + warp; s < S; s += (int64_t)gridDim.x * W) {
-    const int nj = counts ? min(counts[s], J) : J;
+    const int nj = counts ? (int)uni((uint32_t)min(max(counts[s], 0), J)) : J;
     double2 acc[TPL];
 #pragma unroll
     for (int t = 0; t < TPL; ++t) acc[t] = make_double2(0.0, 0.0);
@@ -529,7 +529,7 @@ pool_positions5(const double* __restrict__ xyz, const int32_t* __restrict__ coun
   using G = Pool5Geom<CAP>;
   constexpr int NJ = G::kNJ, NB = G::kNB, MT = G::kMT, NT = G::kNT, C1 = G::kC1, W = G::kW;
   extern __shared__ __align__(16) unsigned char psm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (int)uni(threadIdx.x >> 5);  // warp-uniform, told to the compiler
   double2* Y = reinterpret_cast<double2*>(psm + G::kWarpBytes * warp);  // [kRows][NJ]
   double* WR = reinterpret_cast<double*>(Y + G::kRows * NJ);            // [MT * 8][NJ]
   int2* ocol = reinterpret_cast<int2*>(psm + G::kWarpBytes * W);        // [MT][NT][32]
@@ -559,7 +559,7 @@ pool_positions5(const double* __restrict__ xyz, const int32_t* __restrict__ coun
   __syncthreads();
   const double inv_span = 1.0 / (r_cut - r_in);
   for (int64_t s = (int64_t)blockIdx.x * W + warp; s < S; s += (int64_t)gridDim.x * W) {
-    const int nj = counts ? min(max(counts[s], 0), J) : J;
+    const int nj = counts ? (int)uni((uint32_t)min(max(counts[s], 0), J)) : J;
     double acc[MT][NT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)

@@ -358,14 +358,30 @@ struct SeedsQ {
     }
     return s;
   }
+  // a seed of either class (inner nodes, roots): every path loads into the
+  // same raw words, so the paths merge without register copies
   __device__ __forceinline__ C4 get(uint32_t off, bool hot) const {
+    uint32_t t[16];
     if (hot) {
-      uint32_t t[16];
       hot_issue(off, t);
       tmem_wait_ld();
-      return unpack(t);
+    } else {
+      const uint32_t c = off * 4 - kTmemRowsQ * 2048;  // byte offset of the 2 KB cold row
+      if (!HYB || c < usB) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n"
+                       : "=r"(t[4 * k]), "=r"(t[4 * k + 1]), "=r"(t[4 * k + 2]), "=r"(t[4 * k + 3])
+                       : "r"(sb + c + k * 512));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          asm volatile("ld.global.v4.b32 {%0, %1, %2, %3}, [%4];\n"
+                       : "=r"(t[4 * k]), "=r"(t[4 * k + 1]), "=r"(t[4 * k + 2]), "=r"(t[4 * k + 3])
+                       : "l"(gb + (c - usB) + k * 512));
+      }
     }
-    return cold(off);
+    return unpack(t);
   }
 };
 

@@ -419,7 +419,9 @@ __device__ __forceinline__ void leaf_block_q(const Ring3& st, const C4& pv, doub
 
 // (Round 2: the leaves summed into a chain of their own, apart from the
 // node products, ran cfg4 at 405 k vs 415 k sites/s -- the single site-sum
-// chain is not what binds, and the second one spills at order 6.)
+// chain is not what binds, and the second one spills at order 6.  The Horner
+// form of the leaf level -- G = sum_l c_l s_l, then Re(pv G): 8 DFMA per leaf
+// instead of 12 -- ran 431 k vs 477 k: its 16-register accumulator spills.)
 template <bool HOT, int MAXU, bool HYB>
 __device__ __forceinline__ void leaves_q(Ring3& st, uint32_t n, const C4& pv, double (&acc)[4], const SeedsQ<HYB>& sd,
                                          int lane) {

@@ -130,11 +130,12 @@ int device_labels(int dev, int group, int cap, const int4** out) {
   return 0;
 }
 
-// work chunks per program (ACEDAG_CHUNKS overrides)
+// work chunks per program (ACEDAG_CHUNKS overrides): eight per warp of the
+// 24-warp k2_horner (cfg2 K2: 128 chunks 1.778 ms, 192 1.753, 256 1.754, 384 1.773)
 int plan_chunks() {
   static int c = [] {
     const char* e = getenv("ACEDAG_CHUNKS");
-    int v = e ? atoi(e) : 128;
+    int v = e ? atoi(e) : 192;
     return v < 1 ? 1 : (v > 8192 ? 8192 : v);
   }();
   return c;

@@ -851,11 +851,16 @@ k2_horner(const typename HTr<T>::V* __restrict__ Tab, int64_t S, int U, int us, 
 }  // namespace hdev
 
 // ------------------------------------------------------------------- host
-// warps per CTA: fp64 16 (128 registers; 20 and 24 warps spill and ran
-// 7% / 17% slower at cfg2 -- again in round 2 with the site sums moved to
-// memory to cut the spills: 2.25 / 2.29 vs 2.07 ms); fp32 32 for order <= 4 (64 registers; 1.39 vs
-// 1.58 ms at 16, cfg2), 16 above (one more accumulator per level; 20 ran
-// 611 vs 528 ms at cfg4).  ACEDAG_HWARPS32 = 16 | 32 overrides for fp32.
+// warps per CTA.  fp64, order <= 4: 24 x 80 registers since the walk is
+// declared warp-uniform (the uniform datapath took the control state out of
+// the vector registers: 126 -> 116 unconstrained, and at 80 ptxas spills only
+// three of the four site sums, touched once per root): cfg2 K2 1.877 -> 1.776
+// ms.  (20 warps x 96 registers: 2.49 ms -- 228 B of spills inside the loops;
+// 28 x 72: 2.17 ms; 32 x 64: 2.81 ms.  Before the uniform walk 20 and 24
+// warps ran 7% / 17% slower than 16.)  fp64 above order 4: 16.  fp32: 32 for
+// order <= 4 (64 registers; 1.39 vs 1.58 ms at 16, cfg2), 16 above (one more
+// accumulator per level; 20 ran 611 vs 528 ms at cfg4).  ACEDAG_HWARPS32 = 16
+// | 32 overrides for fp32.
 int horner_warps(bool f32, int nu) {
   static int w32 = [] {
     const char* e = getenv("ACEDAG_HWARPS32");
@@ -865,7 +870,7 @@ int horner_warps(bool f32, int nu) {
   // (fp64 order 5-6 at 12 warps / 170 registers -- no spills -- still ran
   // cfg4 at 150 k vs 415 k sites/s for k2_quad: the deep inner levels, not
   // the registers, are what make Horner slow there; k2_quad stays)
-  if (!f32) return kHornerWarps;
+  if (!f32) return nu <= 4 ? kHornerWarps : 16;
   if (w32) return w32;
   return nu <= 4 ? 32 : 16;
 }
@@ -1162,6 +1167,7 @@ static cudaError_t launch_nu(const void* Tab, int64_t S, int U, int us, const Op
                              double* tail, int grid, cudaStream_t st) {
   const int W = horner_warps(sizeof(T) == 4, NU);
   auto k = hdev::k2_horner<NU, T, HYB, 16>;
+  if constexpr (sizeof(T) == 8 && NU <= 4) k = hdev::k2_horner<NU, T, HYB, kHornerWarps>;
   if constexpr (sizeof(T) == 4) {
     if (W == 32) k = hdev::k2_horner<NU, T, HYB, 32>;
   }

@@ -41,7 +41,7 @@ struct alignas(16) OpH {
 constexpr uint32_t kHornerHot = 32;      // TMEM rows (4 sites x c128 = 16 columns each; c64: 64 rows)
 inline int horner_hot_rows(bool f32) { return f32 ? 64 : (int)kHornerHot; }
 inline int horner_row_bytes(bool f32) { return f32 ? 1024 : 2048; }
-constexpr int kHornerWarps = 16;
+constexpr int kHornerWarps = 24;         // fp64, order <= 4 (16 above; fp32: horner_warps())
 constexpr uint32_t kHornerRing = 2048;   // per-warp program ring: 3 blocks + mirror
 // leaves per record group: a node of the last inner order with more is split
 // into copies of the same seed (the first carrying its coefficient), so a

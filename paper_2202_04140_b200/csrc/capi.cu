@@ -776,14 +776,21 @@ bool tile_seeds(acedag_plan* P, const V* A, int64_t S, int L, const uint16_t* sl
 
 // geometry of k2_quad: 128-site tiles, 32 hot rows in TMEM, 2 KB cold rows
 // in shared memory, the tail read in place from the tile-major table
+// warps per k2_quad CTA: since the walk is declared warp-uniform more warps
+// at fewer registers win (cfg4, 4e4 sites: 16 x 128 registers 482 k sites/s,
+// 20 x 96 531 k, 24 x 80 574 k, 28 x 72 568 k, 32 x 64 570 k)
+#ifndef ACEDAG_QUAD_WARPS
+#define ACEDAG_QUAD_WARPS 24
+#endif
+constexpr int kQuadWarps = ACEDAG_QUAD_WARPS;
 int quad_launch(acedag_plan* P, int64_t S, Launch& lc) {
   const int64_t ntiles = (S + 127) / 128;
-  lc.block = 16 * 32;
+  lc.block = kQuadWarps * 32;
   lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, P->sms - t_sm_reserve));
   lc.rows = P->U + 1;
   const int cold = std::max(0, lc.rows - (int)dev::kTmemRowsQ);
   // rings, TMEM slot + chunk counter (16 B), slot -> label table
-  const size_t fixed = (size_t)16 * dev::Ring3::kAlloc + 16 + (((size_t)lc.rows * 4 + 15) & ~(size_t)15);
+  const size_t fixed = (size_t)kQuadWarps * dev::Ring3::kAlloc + 16 + (((size_t)lc.rows * 4 + 15) & ~(size_t)15);
   const int us_max = (int)((P->smem_optin - fixed) / 2048);
   lc.us = std::min(cold, us_max);
   lc.hyb = lc.us < cold;
@@ -794,7 +801,7 @@ int quad_launch(acedag_plan* P, int64_t S, Launch& lc) {
 template <int NU, bool HYB>
 cudaError_t launch_quad_k(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,
                           double* out, const Launch& lc, cudaStream_t st) {
-  constexpr int W = 16;
+  constexpr int W = kQuadWarps;
   constexpr int MAXU = NU <= 4 ? 2 : 1;
   cudaError_t e;
   if (!tile_seeds<128>(P, A, S, L, slot_label, lc.ws, st, e)) return cudaErrorInvalidValue;
@@ -879,7 +886,10 @@ bool use_horner(const acedag_plan* P, bool f32 = false) {
   return k2_mode() == 2 || (k2_mode() == 0 && P->host.max_order <= 4);
 }
 
-constexpr int kMmaWarps = 16;
+#ifndef ACEDAG_MMA_WARPS
+#define ACEDAG_MMA_WARPS 16
+#endif
+constexpr int kMmaWarps = ACEDAG_MMA_WARPS;
 
 template <int NU, bool HYB>
 cudaError_t launch_mma(acedag_plan* P, const double2* A, int64_t S, int L, const uint16_t* slot_label,

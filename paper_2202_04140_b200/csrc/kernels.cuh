@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(512) k_tile_seeds(const V* __restrict__ A, int
 // amortised twice as far.  Seed rows are 2 KB ([4][32] c128): the 32 hottest
 // in TMEM (16 columns per lane, one x16 load per fetch, replicated per lane
 // quadrant), the next in shared memory, the tail in the per-CTA global
-// cache.  16 warps x 128 registers.
+// cache.  24 warps x 80 registers (capi.cu kQuadWarps).
 constexpr uint32_t kTmemRowsQ = 32;
 
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&r)[16]) {

@@ -897,16 +897,18 @@ double guided_tail() {
 // record costs 1 (leaf) or cost_w(1) (node), a root unit cost_w(2) more);
 // measured at cfg2 (node, root, shared, global): (3, 2, 0, 0) 2.115 ms,
 // (3, 2, 1, 10) 2.081, (2, 4, 0.5, 8) 2.071, (3, 8, 1, 10) 2.102 -- a chunk's
-// real time follows its L2 fetches.  ACEDAG_HCOST_S / ACEDAG_HCOST_G override.
+// real time follows its L2 fetches.  Re-tuned for the 24-warp kernel with
+// same-shape runs: (1.5, 8, 2, 8) 1.729 ms vs (2, 4, 0.5, 8) 1.754.
+// ACEDAG_HCOST_S / ACEDAG_HCOST_G override.
 // record weights: [1] a node record (leaf = 1), [2] extra per root unit
 // (ACEDAG_HCOST_N / ACEDAG_HCOST_R)
 double cost_w(int which) {
-  static double wn = [] { const char* e = getenv("ACEDAG_HCOST_N"); return e ? atof(e) : 2.0; }();
-  static double wr = [] { const char* e = getenv("ACEDAG_HCOST_R"); return e ? atof(e) : 4.0; }();
+  static double wn = [] { const char* e = getenv("ACEDAG_HCOST_N"); return e ? atof(e) : 1.5; }();
+  static double wr = [] { const char* e = getenv("ACEDAG_HCOST_R"); return e ? atof(e) : 8.0; }();
   return which == 1 ? wn : wr;
 }
 double class_cost(uint8_t cls) {
-  static double ws = [] { const char* e = getenv("ACEDAG_HCOST_S"); return e ? atof(e) : 0.5; }();
+  static double ws = [] { const char* e = getenv("ACEDAG_HCOST_S"); return e ? atof(e) : 2.0; }();
   static double wg = [] { const char* e = getenv("ACEDAG_HCOST_G"); return e ? atof(e) : 8.0; }();
   return cls == 1 ? ws : (cls == 2 ? wg : 0.0);
 }

@@ -112,6 +112,21 @@ int ensure_norms(int dev) {
   recip[0] = 0.0;
   for (int k = 1; k < ACEDAG_YLM_LMAX + 2; ++k) recip[k] = 1.0 / k;
   CK(cudaMemcpyToSymbol(dev::c_recip, recip, sizeof(recip)));
+  // three-term recurrence of the NORMALISED functions Q_l^m = N_lm P_l^m:
+  //   Q_l^m = A_lm cos(theta) Q_{l-1}^m - B_lm Q_{l-2}^m
+  // A_lm = (2l-1)/(l-m) N_lm/N_{l-1,m}, B_lm = (l+m-1)/(l-m) N_lm/N_{l-2,m}
+  {
+    constexpr int n = (ACEDAG_YLM_LMAX + 1) * (ACEDAG_YLM_LMAX + 2) / 2;
+    std::vector<double> ra(n, 0.0), rb(n, 0.0);
+    auto idx = [](int l, int m) { return l * (l + 1) / 2 + m; };
+    for (int l = 1; l <= ACEDAG_YLM_LMAX; ++l)
+      for (int m = 0; m < l; ++m) {
+        ra[idx(l, m)] = (2.0 * l - 1.0) / (l - m) * (kYlmNorm[idx(l, m)] / kYlmNorm[idx(l - 1, m)]);
+        if (l - 2 >= m) rb[idx(l, m)] = (l + m - 1.0) / (l - m) * (kYlmNorm[idx(l, m)] / kYlmNorm[idx(l - 2, m)]);
+      }
+    CK(cudaMemcpyToSymbol(dev::c_ylm_a, ra.data(), n * sizeof(double)));
+    CK(cudaMemcpyToSymbol(dev::c_ylm_b, rb.data(), n * sizeof(double)));
+  }
   g_norms_ready[dev] = true;
   return 0;
 }

@@ -22,6 +22,10 @@ namespace dev {
 
 __constant__ double c_ylm_norm[(ACEDAG_YLM_LMAX + 1) * (ACEDAG_YLM_LMAX + 2) / 2];
 __constant__ double c_recip[ACEDAG_YLM_LMAX + 2];  // 1/k, k = 0..LMAX+1 (entry 0 unused)
+// recurrence of the normalised Q_l^m = N_lm P_l^m (capi.cu ensure_norms):
+// Q_l^m = c_ylm_a[l,m] cos(theta) Q_{l-1}^m - c_ylm_b[l,m] Q_{l-2}^m
+__constant__ double c_ylm_a[(ACEDAG_YLM_LMAX + 1) * (ACEDAG_YLM_LMAX + 2) / 2];
+__constant__ double c_ylm_b[(ACEDAG_YLM_LMAX + 1) * (ACEDAG_YLM_LMAX + 2) / 2];
 
 __device__ __forceinline__ double cheb_exact(int k, double x) {  // special.py:19-28
   if (k == 0) return 1.0;
@@ -502,7 +506,10 @@ struct Pool5Geom {
   static constexpr int kNT = (2 * kNP + 7) / 8;                      // 8-column tiles of (re, im)
   static constexpr int kRows = kNT * 4;                              // pair rows incl. padding
   static constexpr size_t kWarpBytes = (size_t)kRows * kNJ * 16 + (size_t)kMT * 8 * kNJ * 8;
-  static constexpr int kW = 8;                                       // warps per CTA (255 registers)
+  // warps per CTA: as many as shared memory holds (19.2 KB per warp at cap
+  // 12, 23 KB at cap 14); ptxas needs ~165 registers, so 11 x 184 / 9 x 224
+  // fit without spills (cfg3 pool: 8 warps 8.35 ms per 1e6 sites, 10 8.08, 11 7.67)
+  static constexpr int kW = CAP <= 12 ? 11 : 9;
   static constexpr size_t kOutBytes = (size_t)kMT * kNT * 32 * 8;    // per-lane output columns
   static constexpr size_t kSmem = (size_t)kW * kWarpBytes + kOutBytes;
   // pair index of (l, m), m-major (m = 0 first): l from m to CAP - m
@@ -600,19 +607,25 @@ pool_positions5(const double* __restrict__ xyz, const int32_t* __restrict__ coun
               ec = nc;
               pmm *= -(2.0 * m - 1.0) * st;
             }
-            double nv = c_ylm_norm[m * (m + 1) / 2 + m] * pmm;
-            Y[G::pair(m, m) * NJ + jl] = make_double2(nv * ec, nv * es);
+            // the recurrence runs on the finished values Y = N P e^{i m phi}
+            // (the phase is constant in l): five FP64 operations per (l, m)
+            // pair instead of eight
+            const double q0 = c_ylm_norm[m * (m + 1) / 2 + m] * pmm;
+            double r0 = q0 * ec, i0 = q0 * es;
+            Y[G::pair(m, m) * NJ + jl] = make_double2(r0, i0);
             if (m + 1 <= CAP - m) {
-              double p0 = pmm, p1 = ct * (2.0 * m + 1.0) * pmm;
-              nv = c_ylm_norm[(m + 1) * (m + 2) / 2 + m] * p1;
-              Y[G::pair(m + 1, m) * NJ + jl] = make_double2(nv * ec, nv * es);
+              const double a1 = c_ylm_a[(m + 1) * (m + 2) / 2 + m] * ct;
+              double r1 = a1 * r0, i1 = a1 * i0;
+              Y[G::pair(m + 1, m) * NJ + jl] = make_double2(r1, i1);
 #pragma unroll
               for (int l = m + 2; l <= CAP - m; ++l) {
-                const double p2 = (ct * (2.0 * l - 1.0) * p1 - (l + m - 1.0) * p0) * c_recip[l - m];
-                nv = c_ylm_norm[l * (l + 1) / 2 + m] * p2;
-                Y[G::pair(l, m) * NJ + jl] = make_double2(nv * ec, nv * es);
-                p0 = p1;
-                p1 = p2;
+                const double al = c_ylm_a[l * (l + 1) / 2 + m] * ct, bl = c_ylm_b[l * (l + 1) / 2 + m];
+                const double r2 = al * r1 - bl * r0, i2 = al * i1 - bl * i0;
+                Y[G::pair(l, m) * NJ + jl] = make_double2(r2, i2);
+                r0 = r1;
+                i0 = i1;
+                r1 = r2;
+                i1 = i2;
               }
             }
           }

@@ -523,30 +523,7 @@ __device__ __forceinline__ void run1(RingH& st, uint32_t n, C4<T>& Hp, const See
     uint32_t q = st.p;
     const uint32_t qe = q + m * 32u;
 #pragma unroll 1
-    for (; q + 32 < qe; q += 64) {
-      const int4 ra = lds128(q), la = lds128(q + 16), rb = lds128(q + 32), lb = lds128(q + 48);
-      typename SD::Tm tla, tlb;
-      sd.hot((uint32_t)la.z, tla);
-      sd.hot((uint32_t)lb.z, tlb);
-      C4<T> spa, spb, H;
-      if constexpr (PC == 0) {
-        typename SD::Tm tpa, tpb;
-        sd.hot((uint32_t)ra.z, tpa);
-        sd.hot((uint32_t)rb.z, tpb);
-        tmem_wait_ld();
-        spa = SD::unpack(tpa);
-        spb = SD::unpack(tpb);
-      } else {
-        spa = seed_of<PC>(sd, (uint32_t)ra.z);
-        spb = seed_of<PC>(sd, (uint32_t)rb.z);
-        tmem_wait_ld();
-      }
-      axpy_init(H, rec_c<T>(ra), rec_c<T>(la), SD::unpack(tla));
-      cmac(Hp, spa, H);
-      axpy_init(H, rec_c<T>(rb), rec_c<T>(lb), SD::unpack(tlb));
-      cmac(Hp, spb, H);
-    }
-    if (q < qe) {
+    for (; q < qe; q += 32) {
       const int4 r = lds128(q), l = lds128(q + 16);
       typename SD::Tm tl;
       sd.hot((uint32_t)l.z, tl);

@@ -504,12 +504,15 @@ struct Pool5Geom {
   static constexpr int kMT = (kC1 + 7) / 8;                          // 8-row tiles of n
   static constexpr int kNP = (CAP / 2 + 1) * (CAP + 1 - CAP / 2);    // pairs with l + m <= CAP
   static constexpr int kNT = (2 * kNP + 7) / 8;                      // 8-column tiles of (re, im)
-  static constexpr int kRows = kNT * 4;                              // pair rows incl. padding
-  static constexpr size_t kWarpBytes = (size_t)kRows * kNJ * 16 + (size_t)kMT * 8 * kNJ * 8;
-  // warps per CTA: as many as shared memory holds (19.2 KB per warp at cap
-  // 12, 23 KB at cap 14); ptxas needs ~165 registers, so 11 x 184 / 9 x 224
+  // table rows kept in shared memory: the padding rows of the last tiles
+  // (n past CAP, pairs past kNP) all read ONE zero row
+  static constexpr int kRows = kNP < kNT * 4 ? kNP + 1 : kNT * 4;    // pair rows (+ the zero row)
+  static constexpr int kWRows = kC1 < kMT * 8 ? kC1 + 1 : kMT * 8;   // radial rows (+ the zero row)
+  static constexpr size_t kWarpBytes = (size_t)kRows * kNJ * 16 + (size_t)kWRows * kNJ * 8;
+  // warps per CTA: as many as shared memory holds (18.2 KB per warp at cap
+  // 12, 22.9 KB at cap 14); ptxas needs ~165 registers, so 12 x 168 / 9 x 224
   // fit without spills (cfg3 pool: 8 warps 8.35 ms per 1e6 sites, 10 8.08, 11 7.67)
-  static constexpr int kW = CAP <= 12 ? 11 : 9;
+  static constexpr int kW = CAP <= 12 ? 12 : 9;
   static constexpr size_t kOutBytes = (size_t)kMT * kNT * 32 * 8;    // per-lane output columns
   static constexpr size_t kSmem = (size_t)kW * kWarpBytes + kOutBytes;
   // pair index of (l, m), m-major (m = 0 first): l from m to CAP - m
@@ -631,11 +634,11 @@ pool_positions5(const double* __restrict__ xyz, const int32_t* __restrict__ coun
           }
         } else {  // K padding of a short pass: zero weights and finite values
 #pragma unroll
-          for (int n = 0; n < MT * 8; ++n) WR[n * NJ + jl] = 0.0;
+          for (int n = 0; n < G::kWRows; ++n) WR[n * NJ + jl] = 0.0;
           for (int q = 0; q < G::kRows; ++q) Y[q * NJ + jl] = make_double2(0.0, 0.0);
         }
-      } else if (j0 == 0) {  // rows of n past CAP and pair rows past kNP: zero once per site
-        for (int q = lane - NB; q < (MT * 8 - C1) * NB; q += 32 - NB)
+      } else if (j0 == 0) {  // the zero rows (n past CAP, pairs past kNP): once per site
+        for (int q = lane - NB; q < (G::kWRows - C1) * NB; q += 32 - NB)
           WR[(C1 + q / NB) * NJ + q % NB] = 0.0;
         for (int q = lane - NB; q < (G::kRows - G::kNP) * NB; q += 32 - NB)
           Y[(G::kNP + q / NB) * NJ + q % NB] = make_double2(0.0, 0.0);
@@ -647,11 +650,17 @@ pool_positions5(const double* __restrict__ xyz, const int32_t* __restrict__ coun
         const int jj = ks * 4 + (lane & 3);
         double a[MT];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) a[mt] = WR[(mt * 8 + (lane >> 2)) * NJ + jj];
+        for (int mt = 0; mt < MT; ++mt) {
+          int row = mt * 8 + (lane >> 2);
+          if (mt == MT - 1) row = min(row, G::kWRows - 1);  // padding rows -> the zero row
+          a[mt] = WR[row * NJ + jj];
+        }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int col = nt * 8 + (lane >> 2);
-          const double b = reinterpret_cast<const double*>(Y + (col >> 1) * NJ + jj)[col & 1];
+          int pr = col >> 1;
+          if (nt == NT - 1) pr = min(pr, G::kRows - 1);  // padding pairs -> the zero row
+          const double b = reinterpret_cast<const double*>(Y + pr * NJ + jj)[col & 1];
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt][nt], a[mt], b);
         }

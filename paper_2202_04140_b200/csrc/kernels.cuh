@@ -655,7 +655,7 @@ __global__ void k_tail_reduce(const double* __restrict__ tailbuf, int64_t first_
 // FP64 tensor cores (mma.sync m8n8k4 f64).  Each warp stages the real parts
 // of its last 8 nodes in shared memory ([8][36] doubles, lane = site); every
 // 4 nodes one k-step of 4 (sites) x 4 (outputs) m8n8k4 tiles accumulates
-// into registers.  Coefficient fragments are prefetched two groups ahead.
+// into registers.  Coefficient fragments are prefetched three groups ahead.
 struct MmaSink {
   static constexpr int kNT = 4;       // n-tiles per pass (32 outputs)
   static constexpr int kStride = 36;  // doubles per staged node row (bank spread)
@@ -671,7 +671,13 @@ struct MmaSink {
   // register prefetch only covers L2 latency, not DRAM
   static constexpr int kPfRecords = 64;
   double acc[4][kNT][2];
-  double bnext[2][kNT];  // B fragments of the next two groups
+  // coefficient groups in flight in registers (cfg5 at 2e4 sites: 2 groups
+  // 220.5 k sites/s, 3 229.1 k, 4 spills: 186.2 k)
+#ifndef ACEDAG_MMA_DEPTH
+#define ACEDAG_MMA_DEPTH 3
+#endif
+  static constexpr int kDepth = ACEDAG_MMA_DEPTH;
+  double bnext[kDepth][kNT];  // B fragments of the next kDepth groups
 
   __device__ __forceinline__ void loadB(double (&b)[kNT], int64_t grp_rec) const {
     const double* row = cre + (grp_rec + (lane & 3)) * n_out + o0 + (lane >> 2);
@@ -687,8 +693,8 @@ struct MmaSink {
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(cre + r0 * n_out), "r"((uint32_t)(n * n_out * 8))
                      : "memory");
     }
-    loadB(bnext[0], rec0);
-    loadB(bnext[1], rec0 + 4);
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) loadB(bnext[d], rec0 + 4 * d);
   }
   __device__ __forceinline__ void store(double re) {
     reinterpret_cast<double*>(g_smem + stg)[(cnt & 7u) * kStride + lane] = re;
@@ -703,9 +709,10 @@ struct MmaSink {
 #pragma unroll
     for (int n = 0; n < kNT; ++n) {
       b[n] = bnext[0][n];
-      bnext[0][n] = bnext[1][n];
+#pragma unroll
+      for (int d = 0; d + 1 < kDepth; ++d) bnext[d][n] = bnext[d + 1][n];
     }
-    loadB(bnext[1], rec0 + done + 8);
+    loadB(bnext[kDepth - 1], rec0 + done + 4 * kDepth);
     done += 4;
     if (lane == 0) {
       const int64_t r = rec0 + done + kPfRecords;

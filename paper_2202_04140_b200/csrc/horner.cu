@@ -7,8 +7,8 @@
 // tcgen05.ld.32x32b.x16 per fetch; fp32: 64 rows of 8 columns; replicated in
 // the four lane quadrants), the next `us` rows in shared memory ([row][4][32],
 // conflict-free 16-B or 8-B loads), the tail read in place from the
-// tile-major table (L2).  fp64 runs 16 warps x 128 registers, fp32 32 x 64
-// (16 above order 4).
+// tile-major table (L2).  fp64 runs 24 warps x 80 registers up to order 4
+// (16 x 128 above), fp32 32 x 64 (16 above order 4): horner_warps().
 //
 // Per warp, the program records of a chunk stream global -> a 3-block shared
 // ring (cp.async, one 512-B block per refill) whose block 0 is mirrored past
@@ -24,10 +24,13 @@
 // Where the time goes (cfg2, tools/mkvariant.sh -DHX_NOFMA / -DHX_NOSEED /
 // -DHX_NOGL timing builds): with the FMAs and the seed fetches both removed
 // the walk alone still takes 1.29 of 2.02 ms; the FMAs add 0.45 ms, the
-// global tail 0.13 ms.  Time follows the instruction count at ~0.55
-// instructions per clock per scheduler (four in-order warps of dependent
-// control code), so the order-4 program sorts each root's children into
-// same-shape runs that are walked by branch-free loops (run1 / run2).
+// global tail 0.13 ms (measured at 16 warps).  Time follows the instruction
+// count at 0.5-0.6 instructions per clock per scheduler (a few in-order warps
+// of dependent control code), so: the walk is declared warp-uniform to the
+// compiler (uni()), which removes the divergence bookkeeping and moves the
+// control state to the uniform registers -- that is what lets 24 warps fit;
+// and the order-4 program sorts each root's children into same-shape runs
+// that are walked by branch-free loops (run1 / run2).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
